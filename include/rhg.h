@@ -1,0 +1,162 @@
+/*
+ * rhg.h -- C-ABI of the B200-native threshold random-hyperbolic-graph generator
+ *          (hot path of Algorithm 1, arXiv 1606.09481).
+ *
+ * Model: n points in the hyperbolic disk D_R, angle
+ * phi ~ U[0, 2pi), radius with density
+ * f(r) = alpha sinh(alpha r) / (cosh(alpha R) - 1) (Eq. 1),
+ * alpha = (gamma - 1)/2.  Vertices u != v are adjacent iff their
+ * hyperbolic distance (Eq. 3) is <= R (T = 0).
+ *
+ * Everything below is plain C: pointers, sizes, status codes.  No torch types.
+ * A `rhg_stream` is a `cudaStream_t` (both are `struct CUstream_st *`); NULL is
+ * the legacy default stream.
+ *
+ * Error behaviour: every entry point validates its arguments first and returns
+ * a status without touching any buffer on RHG_ERR_INVALID / RHG_ERR_CALIBRATION /
+ * RHG_ERR_WORKSPACE.  CUDA failures return RHG_ERR_CUDA; the stream may then hold
+ * partially written outputs.  No entry point allocates device or host memory
+ * beyond a few bytes of pinned host scratch held for the library's lifetime;
+ * all large buffers are caller-owned.
+ */
+#ifndef RHG_H
+#define RHG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *rhg_stream;
+
+typedef enum {
+  RHG_OK = 0,
+  RHG_ERR_INVALID = 2,     /* bad argument: n < 2 or n >= 2^32, kbar <= 0, gamma <= 2 (alpha <= 1/2,
+                              PAPER.md:78), non-finite input, NULL required pointer */
+  RHG_ERR_CALIBRATION = 3, /* getTargetRadius could not bracket kbar on the decreasing branch of
+                              Eq. 22 */
+  RHG_ERR_WORKSPACE = 4,   /* workspace smaller than rhg_workspace_bytes() asks for */
+  RHG_ERR_CAPACITY = 5,    /* output capacity too small; *num_edges holds the required count and
+                              the edge buffers are untouched.  Output is deterministic, so the
+                              caller may reallocate and call again. */
+  RHG_ERR_DOMAIN = 6,      /* an input point has r outside [0, R] or theta outside [0, 2pi)
+                              (SPEC.md:199), detected on the device */
+  RHG_ERR_CUDA = 7         /* a CUDA launch or runtime call failed */
+} rhg_status;
+
+typedef enum {
+  /* Compressed sparse rows over vertex ids 0..n-1: row_ptr[n+1] (uint64),
+     col[row_ptr[n]] (uint32).  Both directions of every edge, no self-loops.
+     Row order is deterministic but unspecified (sort a row to canonicalise). */
+  RHG_CSR = 0,
+  /* Undirected list: pairs[2k], pairs[2k+1] = (u, v), u < v, each edge once.
+     Order deterministic but unspecified. */
+  RHG_EDGES_UNDIRECTED = 1
+} rhg_format;
+
+/* Tuning knobs.  The edge set does not depend on them (DESIGN.md "Why parity is
+   layout-free"); they only move work between window evaluations and tests. */
+typedef struct {
+  int num_bands;     /* L, number of slabs; 0 -> ceil(log2 n) (Z7) */
+  double band_ratio; /* p, geometric width ratio; 0 -> 0.9 */
+  uint32_t heavy_threshold; /* candidates of one (vertex, slab) range above which the range is
+                               split across warps; 0 -> library default */
+  int reserved[5];
+} rhg_options;
+
+/* Per-phase device times (CUDA events on the caller's stream), filled when
+   rhg_output.timing != NULL (adds event records and one extra sync). */
+typedef struct {
+  float ms_sample;   /* K1: Philox point sampling + band assignment            */
+  float ms_sort;     /* K3: segmented radix sort by (band, angle)               */
+  float ms_index;    /* K4: SoA gather + per-band bucket directory              */
+  float ms_count;    /* K5/K7: windows, ranges, certified tests, degrees        */
+  float ms_scan;     /* K6: degree scan -> row offsets                          */
+  float ms_emit;     /* K8: edge emission                                       */
+  float ms_copy;     /* host-buffer mode: device <-> host copies                */
+  float ms_total;    /* first to last event                                     */
+  uint64_t candidates;     /* candidate (vertex, point) tests performed in the count pass */
+  uint64_t launches;       /* kernels launched by this call                                 */
+  uint64_t emit_retested;  /* 1 if the emit pass had to re-run the tests (bit buffer overflow) */
+} rhg_timing;
+
+typedef struct {
+  rhg_format format;
+  /* 0: row_ptr/col/pairs/theta_out/r_out (and the input points of
+     rhg_generate_from_points) are DEVICE pointers.
+     1: they are HOST pointers (page-locked recommended); the library stages the
+        graph in `workspace` and copies it with cudaMemcpyAsync on `stream`. */
+  int host_buffers;
+  uint64_t *row_ptr;       /* CSR: n+1 entries (row_ptr[n] = number of directed edges)        */
+  uint32_t *col;           /* CSR: capacity_edges entries                                      */
+  uint32_t *pairs;         /* EDGES_UNDIRECTED: 2*capacity_edges entries                       */
+  uint64_t capacity_edges; /* CSR: directed entries col can hold; pairs: undirected edges      */
+  void *workspace;         /* device scratch, caller-owned, >= rhg_workspace_bytes(...)        */
+  size_t workspace_bytes;
+  double *theta_out;       /* optional n-array: the sampled angles (generate calls only)       */
+  double *r_out;           /* optional n-array: the sampled radii                              */
+  uint64_t *num_edges;     /* HOST, required: directed count (CSR) or undirected count (pairs);
+                              on RHG_ERR_CAPACITY the required count                          */
+  double *R_used;          /* HOST, optional: the disk radius used                             */
+  const rhg_options *options; /* optional, NULL -> defaults                                    */
+  rhg_timing *timing;      /* HOST, optional                                                  */
+} rhg_output;
+
+/* getTargetRadius: R such that Eq. 22 (zeta = 1) gives kbar,
+   on the decreasing branch (Z5).  Host only. */
+rhg_status rhg_target_radius(uint64_t n, double kbar, double gamma, double *R);
+
+/* Radial slab boundaries c_0..c_L (Eq. 4) the generator uses
+   for n points and disk radius R: writes *L and c[0..L] (c must hold >= 65
+   doubles).  Host only. */
+rhg_status rhg_band_boundaries(uint64_t n, double R, const rhg_options *opt, int *L, double *c);
+
+/* Device scratch needed by the generate calls for n points, output `format`,
+   `capacity_edges` (as in rhg_output) and buffer kind (host_buffers as in
+   rhg_output).  Includes a candidate-bit buffer sized from capacity_edges; if it
+   proves too small at run time the emit pass re-runs the tests instead
+   (slower, same output). */
+size_t rhg_workspace_bytes(uint64_t n, rhg_format format, uint64_t capacity_edges,
+                           int host_buffers);
+
+/* Algorithm 1 end to end: alpha from gamma (line 1), R from
+   getTargetRadius (line 2), then on `stream`: Philox point sampling (lines 7-8;
+   vertex i uses counter i, key = seed, Z12), band assignment (line 9),
+   angular sort per band (lines 11-12), range queries with exact tests (lines
+   13-21), and emission into `out`.  Synchronises once on an 8-byte edge count
+   (capacity check).  Deterministic for fixed (n, kbar, gamma, seed, options). */
+rhg_status rhg_generate(uint64_t n, double kbar, double gamma, uint64_t seed,
+                        const rhg_output *out, rhg_stream stream);
+
+/* Same with the disk radius given directly ("or even accept R directly",
+   PAPER.md:186); alpha > 1/2. */
+rhg_status rhg_generate_with_radius(uint64_t n, double R, double alpha, uint64_t seed,
+                                    const rhg_output *out, rhg_stream stream);
+
+/* Edges of a given point set (Alg. 1 lines 9-21): theta[n] in [0, 2pi),
+   r[n] in [0, R], fp64, device pointers (host if out->host_buffers).  Ids are
+   the input indices.  Out-of-domain points -> RHG_ERR_DOMAIN. */
+rhg_status rhg_generate_from_points(uint64_t n, const double *theta, const double *r, double R,
+                                    const rhg_output *out, rhg_stream stream);
+
+/* K1 alone: write the n sampled points (device pointers) exactly as
+   rhg_generate_with_radius would sample them. */
+rhg_status rhg_sample_points(uint64_t n, double alpha, double R, uint64_t seed, double *theta,
+                             double *r, rhg_stream stream);
+
+/* Raw Philox4x32-10 words for counters i0..i0+count-1 under key = seed
+   (out: device, 4*count uint32).  Exposed for parity tests of the sampler. */
+rhg_status rhg_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t *out,
+                            rhg_stream stream);
+
+const char *rhg_status_string(rhg_status s);
+
+/* Library version string (build id). */
+const char *rhg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RHG_H */

@@ -69,6 +69,9 @@ def lib():
             f.restype = ctypes.c_int64
             f.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double, _u32p, ctypes.c_uint64,
                           _u32p, _u8p, ctypes.c_uint64, _u64p, _u64p]
+        L.orc_sweep_count.restype = ctypes.c_int64
+        L.orc_sweep_count.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double,
+                                      ctypes.c_uint64, ctypes.c_uint64, _u64p]
         L.orc_window.restype = ctypes.c_double
         L.orc_window.argtypes = [ctypes.c_double] * 3
         L.orc_rows.restype = ctypes.c_int64
@@ -208,6 +211,17 @@ def brute_force(theta, r, R, cap_hint=None) -> EdgeSet:
 def sweep(theta, r, R, cap_hint=None) -> EdgeSet:
     n = len(theta)
     return _edge_call(lib().orc_sweep, theta, r, R, cap_hint or 8 * n + 1024)
+
+
+def sweep_count(theta, r, R, id_lo, id_hi):
+    """Edges found from vertices with id in [id_lo, id_hi) (count only), and the
+    number of candidate tests."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    t = ctypes.c_uint64()
+    m = lib().orc_sweep_count(len(theta), _p(theta, _f64p), _p(r, _f64p), R, id_lo, id_hi,
+                              ctypes.byref(t))
+    return int(m), int(t.value)
 
 
 def rows(theta, r, R, queries):

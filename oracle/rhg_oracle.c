@@ -461,6 +461,48 @@ ORC_API int64_t orc_sweep(uint64_t n, const double *theta, const double *r, doub
   return (int64_t)m;
 }
 
+/* (2b) Count-only sweep over the vertices with id in [id_lo, id_hi): edges whose
+ * smaller-(r, id) endpoint lies in the range (same search and decision as (2)).
+ * Used for the bounded CPU baseline timing; *tests receives the number of
+ * candidate pairs decided. */
+ORC_API int64_t orc_sweep_count(uint64_t n, const double *theta, const double *r, double R,
+                                uint64_t id_lo, uint64_t id_hi, uint64_t *tests) {
+  orc_thresh th = orc_make_thresh(R);
+  orc_ang *s = malloc(n * sizeof(orc_ang));
+  for (uint64_t i = 0; i < n; ++i) {
+    s[i].theta = theta[i];
+    s[i].id = (uint32_t)i;
+  }
+  qsort(s, n, sizeof(orc_ang), cmp_ang);
+  uint64_t *pos = malloc(n * sizeof(uint64_t));
+  for (uint64_t k = 0; k < n; ++k) pos[s[k].id] = k;
+  uint64_t m = 0, t = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : m, t)
+  for (int64_t v = (int64_t)id_lo; v < (int64_t)id_hi; ++v) {
+    double rv = r[v];
+    double wpad = orc_window(rv, rv, R) * (1.0 + 1e-9) + 1e-12;
+    int full = wpad >= M_PI;
+    uint64_t p = pos[v];
+    for (int dir = 0; dir < (full ? 1 : 2); ++dir) {
+      for (uint64_t step = 1; step < n; ++step) {
+        uint64_t k = dir == 0 ? (p + step) % n : (p + n - step) % n;
+        const orc_ang *q = &s[k];
+        if (!full && orc_angle_between(theta[v], q->theta) > wpad) break;
+        uint32_t u = q->id;
+        if (u == (uint32_t)v) break;
+        if (r[u] < rv || (r[u] == rv && u < (uint32_t)v)) continue;
+        int tie = 0;
+        m += orc_decide(&th, theta[v], rv, q->theta, r[u], &tie);
+        ++t;
+      }
+    }
+  }
+  free(s);
+  free(pos);
+  if (tests) *tests = t;
+  return (int64_t)m;
+}
+
 /* (3) Neighbourhoods of selected vertices by brute force over all n points
  * (for configurations too large for (1)/(2) in test time).  Writes, for each
  * query k, its neighbour ids (ascending) into nbr[off[k] .. off[k+1]) and

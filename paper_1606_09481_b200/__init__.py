@@ -1,0 +1,306 @@
+"""paper_1606_09481_b200 -- B200-native threshold random-hyperbolic-graph generator.
+
+Thin ctypes binding over ``librhg.so`` (the C-ABI in ``include/rhg.h``).  This
+module only marshals arguments: every step of the method (sampling, band
+assignment, sorting, range queries, tests, emission) runs in the CUDA kernels of
+``csrc/``.  PyTorch is used for device memory and streams only.
+
+There is no CPU fallback: if the extension is missing, importing ``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librhg.so")
+
+RHG_OK, RHG_ERR_INVALID, RHG_ERR_CALIBRATION, RHG_ERR_WORKSPACE = 0, 2, 3, 4
+RHG_ERR_CAPACITY, RHG_ERR_DOMAIN, RHG_ERR_CUDA = 5, 6, 7
+RHG_CSR, RHG_EDGES_UNDIRECTED = 0, 1
+FORMATS = {"csr": RHG_CSR, "edges": RHG_EDGES_UNDIRECTED, "pairs": RHG_EDGES_UNDIRECTED}
+
+# Symbols include/rhg.h declares (tests check they are all exported).
+ABI_SYMBOLS = ("rhg_target_radius", "rhg_band_boundaries", "rhg_workspace_bytes", "rhg_generate",
+               "rhg_generate_with_radius", "rhg_generate_from_points", "rhg_sample_points",
+               "rhg_philox_words", "rhg_status_string", "rhg_version")
+
+
+class RhgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rhg status {status}: {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("num_bands", ctypes.c_int), ("band_ratio", ctypes.c_double),
+                ("heavy_threshold", ctypes.c_uint32), ("reserved", ctypes.c_int * 5)]
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [("ms_sample", ctypes.c_float), ("ms_sort", ctypes.c_float),
+                ("ms_index", ctypes.c_float), ("ms_count", ctypes.c_float),
+                ("ms_scan", ctypes.c_float), ("ms_emit", ctypes.c_float),
+                ("ms_copy", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("candidates", ctypes.c_uint64), ("launches", ctypes.c_uint64),
+                ("emit_retested", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Output(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int), ("host_buffers", ctypes.c_int),
+                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("pairs", ctypes.c_void_p),
+                ("capacity_edges", ctypes.c_uint64), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("theta_out", ctypes.c_void_p),
+                ("r_out", ctypes.c_void_p), ("num_edges", ctypes.POINTER(ctypes.c_uint64)),
+                ("R_used", ctypes.POINTER(ctypes.c_double)),
+                ("options", ctypes.POINTER(Options)), ("timing", ctypes.POINTER(Timing))]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree CUDA library; raise loudly if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        st = ctypes.c_int
+        u64, f64, vp = ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+        L.rhg_target_radius.restype = st
+        L.rhg_target_radius.argtypes = [u64, f64, f64, ctypes.POINTER(f64)]
+        L.rhg_band_boundaries.restype = st
+        L.rhg_band_boundaries.argtypes = [u64, f64, ctypes.POINTER(Options),
+                                          ctypes.POINTER(ctypes.c_int), ctypes.POINTER(f64)]
+        L.rhg_workspace_bytes.restype = ctypes.c_size_t
+        L.rhg_workspace_bytes.argtypes = [u64, ctypes.c_int, u64, ctypes.c_int]
+        L.rhg_generate.restype = st
+        L.rhg_generate.argtypes = [u64, f64, f64, u64, ctypes.POINTER(Output), vp]
+        L.rhg_generate_with_radius.restype = st
+        L.rhg_generate_with_radius.argtypes = [u64, f64, f64, u64, ctypes.POINTER(Output), vp]
+        L.rhg_generate_from_points.restype = st
+        L.rhg_generate_from_points.argtypes = [u64, vp, vp, f64, ctypes.POINTER(Output), vp]
+        L.rhg_sample_points.restype = st
+        L.rhg_sample_points.argtypes = [u64, f64, f64, u64, vp, vp, vp]
+        L.rhg_philox_words.restype = st
+        L.rhg_philox_words.argtypes = [u64, u64, u64, vp, vp]
+        L.rhg_status_string.restype = ctypes.c_char_p
+        L.rhg_status_string.argtypes = [ctypes.c_int]
+        L.rhg_version.restype = ctypes.c_char_p
+        L.rhg_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != RHG_OK:
+        raise RhgError(status, lib().rhg_status_string(status).decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+# --------------------------------------------------------------------------- host math
+def target_radius(n: int, kbar: float, gamma: float) -> float:
+    """getTargetRadius, computed by the library's host code."""
+    R = ctypes.c_double()
+    _check(lib().rhg_target_radius(n, kbar, gamma, ctypes.byref(R)))
+    return R.value
+
+
+def band_boundaries(n: int, R: float, num_bands: int = 0, band_ratio: float = 0.0) -> np.ndarray:
+    o = Options(num_bands, band_ratio, 0)
+    L = ctypes.c_int()
+    c = (ctypes.c_double * 65)()
+    _check(lib().rhg_band_boundaries(n, R, ctypes.byref(o), ctypes.byref(L), c))
+    return np.array(c[: L.value + 1])
+
+
+def workspace_bytes(n: int, fmt: str = "csr", capacity: int = 0, host_buffers: bool = False) -> int:
+    return int(lib().rhg_workspace_bytes(n, FORMATS[fmt], capacity, int(host_buffers)))
+
+
+def version() -> str:
+    return lib().rhg_version().decode()
+
+
+# --------------------------------------------------------------------------- graphs
+@dataclass
+class Graph:
+    n: int
+    format: str
+    R: float
+    num_edges: int                 # directed entries (csr) or undirected edges (pairs)
+    row_ptr: object = None         # torch int64 [n+1] (csr)
+    col: object = None             # torch int32 (bits of uint32) [num_edges] (csr)
+    pairs: object = None           # torch int32 [num_edges, 2] (pairs), u < v
+    theta: object = None
+    r: object = None
+    timing: dict = field(default_factory=dict)
+
+    @property
+    def num_undirected(self) -> int:
+        return self.num_edges // 2 if self.format == "csr" else self.num_edges
+
+
+def _expected_capacity(n, kbar, fmt):
+    if kbar is None:
+        kbar = 16.0
+    m_dir = n * kbar
+    extra = 6.0 * math.sqrt(max(m_dir, 1.0)) + 0.15 * m_dir + 4096
+    return int(m_dir + extra) if fmt == "csr" else int(m_dir / 2 + extra)
+
+
+class Workspace:
+    """Reusable device scratch for repeated calls (the bench keeps one)."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int):
+        torch = _torch()
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspace, stream,
+         host_buffers, want_points, sample, out_bufs=None):
+    torch = _torch()
+    f = FORMATS[fmt]
+    fmt = "csr" if f == RHG_CSR else "pairs"
+    cap = int(capacity) if capacity is not None else _expected_capacity(n, kbar_hint, fmt)
+    opts = Options(0, 0.0, 0) if options is None else Options(
+        int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
+        int(options.get("heavy_threshold", 0)))
+    ws = workspace if workspace is not None else Workspace(device)
+    for attempt in range(2):
+        nbytes = int(lib().rhg_workspace_bytes(n, f, cap, int(host_buffers)))
+        wbuf = ws.get(nbytes)
+        if out_bufs is not None:
+            row_ptr, col, pairs, theta, r = out_bufs(cap)
+        else:
+            kw = dict(device="cpu", pin_memory=True) if host_buffers else dict(device=device)
+            row_ptr = torch.empty(n + 1, dtype=torch.int64, **kw) if f == RHG_CSR else None
+            col = torch.empty(max(cap, 1), dtype=torch.int32, **kw) if f == RHG_CSR else None
+            pairs = torch.empty((max(cap, 1), 2), dtype=torch.int32, **kw) if f != RHG_CSR else None
+            theta = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
+            r = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
+        ne = ctypes.c_uint64()
+        Ru = ctypes.c_double()
+        tm = Timing()
+        out = Output(f, int(host_buffers), _ptr(row_ptr), _ptr(col), _ptr(pairs), cap,
+                     wbuf.data_ptr(), wbuf.numel(), _ptr(theta), _ptr(r), ctypes.pointer(ne),
+                     ctypes.pointer(Ru), ctypes.pointer(opts),
+                     ctypes.pointer(tm) if timing else None)
+        st = call(ctypes.byref(out), _stream_handle(stream))
+        if st == RHG_ERR_CAPACITY and capacity is None and attempt == 0:
+            cap = int(ne.value)
+            continue
+        _check(st)
+        m = int(ne.value)
+        g = Graph(n=n, format=fmt, R=Ru.value, num_edges=m, theta=theta, r=r,
+                  timing=tm.as_dict() if timing else {})
+        if f == RHG_CSR:
+            g.row_ptr, g.col = row_ptr, col[:m]
+        else:
+            g.pairs = pairs[:m]
+        return g
+    raise RuntimeError("unreachable")
+
+
+def generate(n: int, kbar: float, gamma: float, seed: int, fmt: str = "csr", *, device="cuda",
+             capacity=None, options=None, timing=False, workspace=None, stream=None,
+             host_buffers=False, return_points=False) -> Graph:
+    """Algorithm 1 end to end on the GPU."""
+    L = lib()
+    return _run(lambda o, s: L.rhg_generate(n, kbar, gamma, seed, o, s), n, fmt, kbar,
+                device=device, capacity=capacity, options=options, timing=timing,
+                workspace=workspace, stream=stream, host_buffers=host_buffers,
+                want_points=return_points, sample=True)
+
+
+def generate_with_radius(n: int, R: float, alpha: float, seed: int, fmt: str = "csr", *,
+                         device="cuda", capacity=None, options=None, timing=False, workspace=None,
+                         stream=None, host_buffers=False, return_points=False,
+                         kbar_hint=None) -> Graph:
+    """Same with R given directly."""
+    L = lib()
+    return _run(lambda o, s: L.rhg_generate_with_radius(n, R, alpha, seed, o, s), n, fmt,
+                kbar_hint, device=device, capacity=capacity, options=options, timing=timing,
+                workspace=workspace, stream=stream, host_buffers=host_buffers,
+                want_points=return_points, sample=True)
+
+
+def generate_from_points(theta, r, R: float, fmt: str = "csr", *, capacity=None, options=None,
+                         timing=False, workspace=None, stream=None, kbar_hint=None) -> Graph:
+    """Edges of a given point set (fp64 torch tensors; CUDA tensors, or CPU tensors
+    for the host-buffer mode)."""
+    torch = _torch()
+    theta = theta.contiguous()
+    r = r.contiguous()
+    assert theta.dtype == torch.float64 and r.dtype == torch.float64 and theta.shape == r.shape
+    n = theta.numel()
+    host = not theta.is_cuda
+    if host and not theta.is_pinned():
+        theta, r = theta.pin_memory(), r.pin_memory()
+    device = "cuda" if host else theta.device
+    L = lib()
+    hint = kbar_hint if kbar_hint is not None else 16.0
+    return _run(lambda o, s: L.rhg_generate_from_points(n, theta.data_ptr(), r.data_ptr(), R, o, s),
+                n, fmt, hint, device=device, capacity=capacity, options=options, timing=timing,
+                workspace=workspace, stream=stream, host_buffers=host, want_points=False,
+                sample=False)
+
+
+def sample_points(n: int, alpha: float, R: float, seed: int, device="cuda", stream=None):
+    """K1 alone: the points rhg_generate_with_radius(n, R, alpha, seed) uses."""
+    torch = _torch()
+    th = torch.empty(n, dtype=torch.float64, device=device)
+    r = torch.empty(n, dtype=torch.float64, device=device)
+    _check(lib().rhg_sample_points(n, alpha, R, seed, th.data_ptr(), r.data_ptr(),
+                                   _stream_handle(stream)))
+    return th, r
+
+
+def philox_words(seed: int, i0: int, count: int, device="cuda", stream=None):
+    torch = _torch()
+    out = torch.empty((count, 4), dtype=torch.int32, device=device)
+    _check(lib().rhg_philox_words(seed, i0, count, out.data_ptr(), _stream_handle(stream)))
+    return out
+
+
+# --------------------------------------------------------------------------- helpers
+def csr_to_pairs_numpy(row_ptr, col):
+    """(u, v) with u < v from a symmetric CSR (host numpy)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    c = np.asarray(col).view(np.uint32).astype(np.int64)
+    u = np.repeat(np.arange(len(rp) - 1, dtype=np.int64), np.diff(rp))
+    keep = u < c
+    p = np.stack([u[keep], c[keep]], axis=1).astype(np.uint32)
+    key = p[:, 0].astype(np.uint64) << np.uint64(32) | p[:, 1].astype(np.uint64)
+    return p[np.argsort(key, kind="stable")]

@@ -1,0 +1,192 @@
+// k_sample.cu -- K1 (Philox point sampler) and K2 (band assignment, sort keys,
+// band histogram), plus the band-layout kernel.
+//
+// Paper: Alg. 1 lines 6-10: draw phi ~ U[0, 2pi) and r with
+// density f(r) = alpha sinh(alpha r)/(cosh(alpha R) - 1) (Eq. 1),
+// insert into the slab b_i with c_i <= r < c_{i+1}.
+#include "rhg_internal.cuh"
+
+namespace rhg {
+
+// Philox4x32-10 (Salmon et al. 2011): counter (i_lo, i_hi, 0, 0), key = seed.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 vertex_words(uint64_t seed, uint64_t i) {
+  return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
+                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+// theta = fl(2pi) * u1, u1 = (w1:w0 >> 11) 2^-53  (Z10, Z12)
+// r = (2/alpha) asinh(sqrt(u2 * (cosh(alpha R) - 1)/2)), clamped to R (Z11)
+__device__ __forceinline__ void words_to_point(uint4 w, double two_over_alpha, double half_span,
+                                               double R, double& theta, double& r) {
+  uint64_t a = ((uint64_t)w.y << 32) | w.x;
+  uint64_t b = ((uint64_t)w.w << 32) | w.z;
+  double u1 = __dmul_rn((double)(a >> 11), 0x1.0p-53);
+  double u2 = __dmul_rn((double)(b >> 11), 0x1.0p-53);
+  theta = __dmul_rn(RHG_TWO_PI_HI, u1);
+  double rr = __dmul_rn(two_over_alpha, asinh(sqrt(__dmul_rn(u2, half_span))));
+  r = rr > R ? R : rr;
+}
+
+// Band j with c_j <= r < c_{j+1}; the last band is closed at R (Reading Z8).
+__device__ __forceinline__ uint32_t band_of(double r, const BandConst& bc) {
+  int j = bc.L - 1;
+  while (j > 0 && r < bc.c[j]) --j;
+  return (uint32_t)j;
+}
+
+// 27-bit fixed-point angle, monotone non-decreasing in theta.
+__device__ __forceinline__ uint32_t q27_of(double theta) {
+  uint32_t q = __double2uint_rz(__dmul_rn(theta, RHG_Q27_SCALE));
+  return q > kQMax ? kQMax : q;
+}
+
+__global__ void k_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < count;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 w = vertex_words(seed, i0 + t);
+    reinterpret_cast<uint4*>(out)[t] = w;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_sample(uint64_t n, uint64_t seed, double two_over_alpha, double half_span,
+             const __grid_constant__ BandConst bc, double* __restrict__ theta,
+             double* __restrict__ r, uint32_t* __restrict__ keys, uint32_t* __restrict__ idx,
+             uint32_t* __restrict__ band_hist) {
+  __shared__ uint32_t hist[kMaxBands];
+  if (threadIdx.x < kMaxBands) hist[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    double th, rr;
+    words_to_point(vertex_words(seed, i), two_over_alpha, half_span, bc.R, th, rr);
+    if (theta) theta[i] = th;
+    if (r) r[i] = rr;
+    if (keys) {
+      uint32_t j = band_of(rr, bc);
+      keys[i] = (j << kBandShift) | q27_of(th);
+      idx[i] = (uint32_t)i;
+      atomicAdd(&hist[j], 1u);
+    }
+  }
+  __syncthreads();
+  if (keys && threadIdx.x < kMaxBands && hist[threadIdx.x])
+    atomicAdd(&band_hist[threadIdx.x], hist[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256)
+    k_keys_from_points(uint64_t n, const double* __restrict__ theta, const double* __restrict__ r,
+                       const __grid_constant__ BandConst bc, uint32_t* __restrict__ keys,
+                       uint32_t* __restrict__ idx, uint32_t* __restrict__ band_hist,
+                       DevScalars* sc) {
+  __shared__ uint32_t hist[kMaxBands];
+  __shared__ uint32_t bad;
+  if (threadIdx.x < kMaxBands) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    double th = theta[i], rr = r[i];
+    // domain: theta in [0, 2pi), r in [0, R]; NaN fails both
+    bool ok = (th >= 0.0) && (th < RHG_TWO_PI_HI) && (rr >= 0.0) && (rr <= bc.R);
+    if (!ok) {
+      bad = 1;
+      th = 0.0;
+      rr = 0.0;
+    }
+    uint32_t j = band_of(rr, bc);
+    keys[i] = (j << kBandShift) | q27_of(th);
+    idx[i] = (uint32_t)i;
+    atomicAdd(&hist[j], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxBands && hist[threadIdx.x]) atomicAdd(&band_hist[threadIdx.x], hist[threadIdx.x]);
+  if (threadIdx.x == 0 && bad) atomicOr(&sc->domain_error, 1u);
+}
+
+// One warp: band offsets, bucket-directory geometry.  Buckets per band: the
+// power of two >= ceil(n_j / 2) (about 1-2 points per bucket), capped at 2^27.
+__global__ void k_band_layout(int L, const uint32_t* __restrict__ band_hist, BandLayout* lay) {
+  int j = threadIdx.x;
+  uint32_t cnt = (j < L) ? band_hist[j] : 0u;
+  uint32_t nb = 1, sh = kQBits;
+  if (j < L) {
+    uint32_t want = (cnt + 1) / 2;
+    while (nb < want && sh > 0) {
+      nb <<= 1;
+      --sh;
+    }
+  }
+  uint32_t dsz = (j < L) ? nb + 1 : 0u;
+  // inclusive warp scans
+  uint32_t s_cnt = cnt, s_dir = dsz;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t a = __shfl_up_sync(0xffffffffu, s_cnt, o);
+    uint32_t b = __shfl_up_sync(0xffffffffu, s_dir, o);
+    if (j >= o) {
+      s_cnt += a;
+      s_dir += b;
+    }
+  }
+  if (j < L) {
+    lay->count[j] = cnt;
+    lay->start[j] = s_cnt - cnt;
+    lay->dir_off[j] = s_dir - dsz;
+    lay->shift[j] = sh;
+    lay->nb[j] = nb;
+  }
+  if (j == L - 1) {
+    lay->start[L] = s_cnt;
+    lay->dir_off[L] = s_dir;
+  }
+}
+
+static int grid_for(uint64_t n, int threads, int max_blocks) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b > (uint64_t)max_blocks ? max_blocks : b);
+}
+
+cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out,
+                                cudaStream_t st) {
+  k_philox_words<<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(seed, i0, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample(uint64_t n, uint64_t seed, double alpha, double R, const BandConst& bc,
+                          double* theta, double* r, uint32_t* keys, uint32_t* idx,
+                          uint32_t* band_hist, cudaStream_t st) {
+  double half_span = (cosh(alpha * R) - 1.0) / 2.0;
+  k_sample<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, seed, 2.0 / alpha, half_span, bc, theta,
+                                                       r, keys, idx, band_hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const double* r,
+                                    const BandConst& bc, uint32_t* keys, uint32_t* idx,
+                                    uint32_t* band_hist, DevScalars* sc, cudaStream_t st) {
+  k_keys_from_points<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, theta, r, bc, keys, idx,
+                                                                 band_hist, sc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_layout(const BandConst& bc, const uint32_t* band_hist, BandLayout* lay,
+                               cudaStream_t st) {
+  k_band_layout<<<1, 32, 0, st>>>(bc.L, band_hist, lay);
+  return cudaGetLastError();
+}
+
+}  // namespace rhg

@@ -1,0 +1,242 @@
+// k_sort.cu -- K3: stable LSD radix sort of 32-bit keys (band << 27 | q27(theta))
+// with a 32-bit payload, plus the generic exclusive scans (K6).
+//
+// Paper: "sort points in b by their angular coordinates" (Alg. 1 lines 11-12,
+// PAPER.md:153-155).  One global sort by (band, angle) yields every band as a
+// contiguous, angle-sorted segment (the slabs b_i of PAPER.md:192-197).
+#include "rhg_internal.cuh"
+
+namespace rhg {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;                       // per thread
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per block
+constexpr int RS_RADIX = 256;
+
+__global__ void __launch_bounds__(RS_THREADS)
+    k_rs_hist(uint32_t n, const uint32_t* __restrict__ keys, int shift, uint32_t* __restrict__ hist,
+              uint32_t G) {
+  __shared__ uint32_t h[RS_RADIX];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t base = blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    uint32_t i = base + it * RS_THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFFu], 1u);
+  }
+  __syncthreads();
+  hist[threadIdx.x * G + blockIdx.x] = h[threadIdx.x];  // digit-major
+}
+
+// Stable scatter.  Warp w of block b owns items [b*TILE + w*512, +512) and walks
+// them in 16 rounds of 32; __match_any_sync ranks equal digits within a round.
+__global__ void __launch_bounds__(RS_THREADS)
+    k_rs_scatter(uint32_t n, const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                 uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int shift,
+                 const uint32_t* __restrict__ offs, uint32_t G) {
+  __shared__ uint32_t wcnt[RS_WARPS][RS_RADIX];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int d = lane; d < RS_RADIX; d += 32) wcnt[w][d] = 0;
+  __syncwarp();
+  const uint32_t wbase = blockIdx.x * RS_TILE + w * (32 * RS_ITEMS);
+  uint32_t key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    uint32_t i = wbase + it * 32 + lane;
+    bool valid = i < n;
+    key[it] = valid ? kin[i] : 0u;
+    val[it] = valid ? vin[i] : 0u;
+    uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t before = wcnt[w][d & 0xFFu];
+    loc[it] = before + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == lane) wcnt[w][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps (warp order = item order => stable)
+  {
+    int d = threadIdx.x;  // RS_THREADS == RS_RADIX
+    uint32_t run = offs[d * G + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      uint32_t c = wcnt[ww][d];
+      wcnt[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    uint32_t i = wbase + it * 32 + lane;
+    if (i < n) {
+      uint32_t d = (key[it] >> shift) & 0xFFu;
+      uint32_t pos = wcnt[w][d] + loc[it];
+      kout[pos] = key[it];
+      vout[pos] = val[it];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- scans
+constexpr int SC_THREADS = 1024;
+constexpr int SC_ITEMS = 8;
+constexpr int SC_CHUNK = SC_THREADS * SC_ITEMS;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T a = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += a;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive prefix,
+// writes the block total to *total.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T s = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : T(0);
+    T si = warp_incl_scan(s);
+    sh[lane] = si - s;
+    if (lane == 31) sh[32] = si;
+  }
+  __syncthreads();
+  T res = inc - v + sh[w];
+  if (total) *total = sh[32];
+  __syncthreads();
+  return res;
+}
+
+template <typename TIn, typename TAcc>
+__global__ void __launch_bounds__(SC_THREADS)
+    k_scan_reduce(uint64_t n, const TIn* __restrict__ in, TAcc* __restrict__ partial) {
+  __shared__ TAcc sh[33];
+  uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK;
+  TAcc s = 0;
+#pragma unroll
+  for (int it = 0; it < SC_ITEMS; ++it) {
+    uint64_t i = base + (uint64_t)it * SC_THREADS + threadIdx.x;
+    if (i < n) s += (TAcc)in[i];
+  }
+  TAcc tot;
+  block_excl_scan<TAcc>(s, sh, &tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of the partials in place; total -> *total
+template <typename TAcc>
+__global__ void __launch_bounds__(SC_THREADS)
+    k_scan_partials(uint32_t m, TAcc* partial, TAcc* total_slot, unsigned long long* total_out) {
+  __shared__ TAcc sh[33];
+  TAcc carry = 0;
+  for (uint32_t base = 0; base < m; base += SC_THREADS) {
+    uint32_t i = base + threadIdx.x;
+    TAcc v = i < m ? partial[i] : TAcc(0);
+    TAcc tot;
+    TAcc ex = block_excl_scan<TAcc>(v, sh, &tot);
+    if (i < m) partial[i] = ex + carry;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    if (total_slot) *total_slot = carry;
+    if (total_out) *total_out = (unsigned long long)carry;
+  }
+}
+
+// Each thread owns SC_ITEMS consecutive elements (blocked), exclusive scan.
+template <typename TIn, typename TOut, typename TAcc>
+__global__ void __launch_bounds__(SC_THREADS)
+    k_scan_down(uint64_t n, const TIn* __restrict__ in, TOut* __restrict__ out,
+                const TAcc* __restrict__ partial) {
+  __shared__ TAcc sh[33];
+  uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK + (uint64_t)threadIdx.x * SC_ITEMS;
+  TAcc v[SC_ITEMS];
+  TAcc s = 0;
+#pragma unroll
+  for (int it = 0; it < SC_ITEMS; ++it) {
+    uint64_t i = base + it;
+    v[it] = i < n ? (TAcc)in[i] : TAcc(0);
+    s += v[it];
+  }
+  TAcc ex = block_excl_scan<TAcc>(s, sh, (TAcc*)nullptr) + partial[blockIdx.x];
+#pragma unroll
+  for (int it = 0; it < SC_ITEMS; ++it) {
+    uint64_t i = base + it;
+    if (i < n) out[i] = (TOut)ex;
+    ex += v[it];
+  }
+}
+
+static uint32_t sc_blocks(uint64_t n) { return (uint32_t)((n + SC_CHUNK - 1) / SC_CHUNK); }
+
+size_t scan_tmp_bytes(uint64_t n) { return (size_t)(sc_blocks(n) + 2) * sizeof(uint64_t) + 256; }
+
+cudaError_t exclusive_scan_u32_u64(uint32_t n, const uint32_t* in, uint64_t* out, void* tmp,
+                                   unsigned long long* total_out, cudaStream_t st, int* launches) {
+  uint32_t B = sc_blocks(n);
+  if (B == 0) B = 1;
+  uint64_t* partial = (uint64_t*)tmp;
+  k_scan_reduce<uint32_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n, in, partial);
+  k_scan_partials<uint64_t><<<1, SC_THREADS, 0, st>>>(B, partial, out + n, total_out);
+  k_scan_down<uint32_t, uint64_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n, in, out, partial);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+static cudaError_t exclusive_scan_u32_inplace(uint32_t n, uint32_t* data, uint32_t* partial,
+                                              cudaStream_t st, int* launches) {
+  uint32_t B = sc_blocks(n);
+  k_scan_reduce<uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, partial);
+  k_scan_partials<uint32_t><<<1, SC_THREADS, 0, st>>>(B, partial, nullptr, nullptr);
+  k_scan_down<uint32_t, uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, data, partial);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+size_t radix_sort_tmp_bytes(uint64_t n) {
+  uint64_t G = (n + RS_TILE - 1) / RS_TILE;
+  if (G == 0) G = 1;
+  uint64_t H = G * RS_RADIX;
+  return (size_t)(H + sc_blocks(H) + 64) * sizeof(uint32_t) + 256;
+}
+
+cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
+                       uint32_t* vals_b, void* tmp, int begin_bit, int end_bit, cudaStream_t st,
+                       int* launches) {
+  uint32_t G = (n + RS_TILE - 1) / RS_TILE;
+  if (G == 0) return cudaSuccess;
+  uint32_t* hist = (uint32_t*)tmp;
+  uint32_t* partial = hist + (size_t)G * RS_RADIX;
+  uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
+  int passes = 0;
+  for (int sh = begin_bit; sh < end_bit; sh += 8) {
+    k_rs_hist<<<G, RS_THREADS, 0, st>>>(n, ki, sh, hist, G);
+    cudaError_t e = exclusive_scan_u32_inplace(G * RS_RADIX, hist, partial, st, launches);
+    if (e != cudaSuccess) return e;
+    k_rs_scatter<<<G, RS_THREADS, 0, st>>>(n, ki, vi, ko, vo, sh, hist, G);
+    if (launches) *launches += 2;
+    uint32_t* t;
+    t = ki; ki = ko; ko = t;
+    t = vi; vi = vo; vo = t;
+    ++passes;
+  }
+  if (passes & 1) {  // result must land in (keys_a, vals_a)
+    cudaMemcpyAsync(keys_a, ki, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(vals_a, vi, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rhg

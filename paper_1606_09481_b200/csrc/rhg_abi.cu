@@ -1,0 +1,408 @@
+// rhg_abi.cu -- the C-ABI (include/rhg.h): argument validation, host-side model
+// parameters (L0), workspace layout and the launch sequence of Algorithm 1.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "rhg_internal.cuh"
+
+using namespace rhg;
+
+#define RHG_VERSION "rhg-b200 r01"
+
+namespace {
+
+// ------------------------------------------------------------------ L0 math
+// Expected average degree, Krioukov Eq. (22) as printed in PAPER.md:178-182 with
+// zeta = 1:
+//   kbar(R) = 2/pi xi^2 n [ e^{-R/2} + e^{-alpha R} ( alpha R/2 (pi/4 alpha^-2
+//             - (pi-1) alpha^-1 + (pi-2)) - 1 ) ],   xi = alpha / (alpha - 1/2).
+double kbar_of_radius(double n, double alpha, double R) {
+  const double pi = 3.14159265358979323846;
+  const double xi = alpha / (alpha - 0.5);
+  const double inv = 1.0 / alpha;
+  const double poly = (pi / 4.0) * inv * inv - (pi - 1.0) * inv + (pi - 2.0);
+  return (2.0 / pi) * xi * xi * n *
+         (std::exp(-R / 2.0) + std::exp(-alpha * R) * (alpha * R / 2.0 * poly - 1.0));
+}
+
+// getTargetRadius.  kbar(R) rises from 0 at R = 0 to one peak
+// and then falls (Z5); locate the peak by golden-section search, then
+// bisect the falling branch down to adjacent doubles.
+rhg_status target_radius(double n, double kbar, double alpha, double* R) {
+  if (!(alpha > 0.5) || !(kbar > 0.0) || !std::isfinite(kbar) || !(n >= 2.0)) return RHG_ERR_INVALID;
+  double a = 0.0, b = 50.0;
+  const double g = 0.6180339887498949;
+  double x1 = b - g * (b - a), x2 = a + g * (b - a);
+  double f1 = kbar_of_radius(n, alpha, x1), f2 = kbar_of_radius(n, alpha, x2);
+  for (int it = 0; it < 200; ++it) {
+    if (f1 < f2) {
+      a = x1; x1 = x2; f1 = f2; x2 = a + g * (b - a); f2 = kbar_of_radius(n, alpha, x2);
+    } else {
+      b = x2; x2 = x1; f2 = f1; x1 = b - g * (b - a); f1 = kbar_of_radius(n, alpha, x1);
+    }
+  }
+  double lo = 0.5 * (a + b), hi = 10.0 * std::log(n) + 50.0;
+  if (kbar > kbar_of_radius(n, alpha, lo) || kbar < kbar_of_radius(n, alpha, hi))
+    return RHG_ERR_CALIBRATION;
+  while (true) {
+    double mid = lo + 0.5 * (hi - lo);
+    if (!(mid > lo && mid < hi)) break;
+    if (kbar_of_radius(n, alpha, mid) > kbar) lo = mid; else hi = mid;
+  }
+  *R = lo + 0.5 * (hi - lo);
+  return RHG_OK;
+}
+
+int default_bands(uint64_t n) {
+  int L = 0;
+  while (L < 32 && (1ull << L) < n) ++L;  // ceil(log2 n)
+  return L < 1 ? 1 : L;
+}
+
+// Slab boundaries: c_0 = 0, c_1 = (1-p)R/(1-p^L),
+// c_{k+1} - c_k = p (c_k - c_{k-1}), c_L = R.
+void make_boundaries(double R, int L, double p, double* c) {
+  const double c1 = (1.0 - p) * R / (1.0 - std::pow(p, L));
+  double w = c1;
+  c[0] = 0.0;
+  for (int k = 1; k < L; ++k) {
+    c[k] = c[k - 1] + w;
+    w *= p;
+  }
+  c[L] = R;
+}
+
+rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandConst* bc) {
+  int L = (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
+  double p = (opt && opt->band_ratio > 0.0) ? opt->band_ratio : 0.9;
+  if (L < 1 || L > kMaxBands || !(p > 0.0 && p < 1.0)) return RHG_ERR_INVALID;
+  memset(bc, 0, sizeof(*bc));
+  bc->L = L;
+  bc->R = R;
+  const double h = std::sinh(R / 2.0);
+  bc->T4 = 4.0 * h * h;
+  make_boundaries(R, L, p, bc->c);
+  for (int j = 0; j < L; ++j) {
+    bc->A[j] = std::exp(0.5 * bc->c[j]);
+    bc->B[j] = std::exp(-0.5 * bc->c[j]);
+    bc->invS[j] = bc->c[j] > 0.0 ? 1.0 / std::sinh(bc->c[j]) : 0.0;
+  }
+  return RHG_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, dir, deg, offs,
+      scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
+};
+
+Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  L.theta = take(8 * n);
+  L.r = take(8 * n);
+  L.keys_a = take(4 * n);
+  L.vals_a = take(4 * n);
+  L.keys_b = take(4 * n);
+  L.vals_b = take(4 * n);
+  L.sort_tmp = take(radix_sort_tmp_bytes(n));
+  L.hist = take(4 * kMaxBands);
+  L.lay = take(sizeof(BandLayout));
+  L.pts = take(sizeof(PointRec) * n);
+  L.dir = take(4 * (n + 4 * kMaxBands + 8));
+  L.deg = take(4 * n);
+  L.offs = take(8 * (n + 1));
+  L.scan_tmp = take(scan_tmp_bytes(n));
+  L.sc = take(sizeof(DevScalars));
+  L.st_rowptr = host && f == RHG_CSR ? take(8 * (n + 1)) : o;
+  L.st_edges = host ? take(f == RHG_CSR ? 4 * cap : 8 * cap) : o;
+  L.st_in_theta = o;  // host-mode inputs reuse theta / r
+  L.st_in_r = o;
+  L.bits = o;
+  L.total = o;
+  return L;
+}
+
+cudaError_t& last_cuda_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+std::mutex g_pin_mu;
+DevScalars* g_pin = nullptr;  // page-locked readback slot
+
+DevScalars* pinned_scalars() {
+  std::lock_guard<std::mutex> g(g_pin_mu);
+  if (!g_pin) {
+    if (cudaMallocHost(&g_pin, sizeof(DevScalars)) != cudaSuccess) g_pin = nullptr;
+  }
+  return g_pin;
+}
+
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t e__ = (x);                     \
+    if (e__ != cudaSuccess) {                  \
+      last_cuda_error() = e__;                 \
+      return RHG_ERR_CUDA;                     \
+    }                                          \
+  } while (0)
+
+struct Timer {
+  bool on = false;
+  cudaEvent_t ev[9];
+  cudaStream_t st;
+  int n = 0;
+  void init(bool enable, cudaStream_t s) {
+    on = enable;
+    st = s;
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  void mark() {
+    if (on && n < 9) cudaEventRecord(ev[n++], st);
+  }
+  float between(int a, int b) {
+    float ms = 0;
+    if (on && b < n) cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+// The full pipeline.  sample == true: Philox points (alpha, seed); else the
+// caller's points (theta_in, r_in).
+rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const double* theta_in,
+               const double* r_in, double R, const rhg_output* out, cudaStream_t st) {
+  if (!out || !out->num_edges) return RHG_ERR_INVALID;
+  if (n < 2 || n >= (1ull << 32)) return RHG_ERR_INVALID;
+  if (!(R >= 0.0) || !std::isfinite(R)) return RHG_ERR_INVALID;
+  if (sample && (!(alpha > 0.5) || !std::isfinite(std::cosh(alpha * R)))) return RHG_ERR_INVALID;
+  if (!std::isfinite(std::sinh(R / 2.0) * std::sinh(R / 2.0) * 4.0)) return RHG_ERR_INVALID;
+  const rhg_format f = out->format;
+  if (f != RHG_CSR && f != RHG_EDGES_UNDIRECTED) return RHG_ERR_INVALID;
+  const int host = out->host_buffers ? 1 : 0;
+  if (f == RHG_CSR && (!out->row_ptr || (!out->col && out->capacity_edges))) return RHG_ERR_INVALID;
+  if (f == RHG_EDGES_UNDIRECTED && !out->pairs && out->capacity_edges) return RHG_ERR_INVALID;
+  if (!sample && (!theta_in || !r_in)) return RHG_ERR_INVALID;
+  BandConst bc;
+  rhg_status s = make_band_const(n, R, out->options, &bc);
+  if (s != RHG_OK) return s;
+  const Layout Lw = plan_layout(n, f, out->capacity_edges, host);
+  if (!out->workspace || out->workspace_bytes < Lw.total) return RHG_ERR_WORKSPACE;
+  DevScalars* pin = pinned_scalars();
+  if (!pin) return RHG_ERR_CUDA;
+
+  char* ws = (char*)out->workspace;
+  double* theta = (double*)(ws + Lw.theta);
+  double* r = (double*)(ws + Lw.r);
+  uint32_t* keys_a = (uint32_t*)(ws + Lw.keys_a);
+  uint32_t* vals_a = (uint32_t*)(ws + Lw.vals_a);
+  uint32_t* keys_b = (uint32_t*)(ws + Lw.keys_b);
+  uint32_t* vals_b = (uint32_t*)(ws + Lw.vals_b);
+  uint32_t* hist = (uint32_t*)(ws + Lw.hist);
+  BandLayout* lay = (BandLayout*)(ws + Lw.lay);
+  PointRec* pts = (PointRec*)(ws + Lw.pts);
+  uint32_t* dir = (uint32_t*)(ws + Lw.dir);
+  uint32_t* deg = (uint32_t*)(ws + Lw.deg);
+  uint64_t* offs_ws = (uint64_t*)(ws + Lw.offs);
+  DevScalars* sc = (DevScalars*)(ws + Lw.sc);
+  uint64_t* row_ptr_dev = host ? (uint64_t*)(ws + Lw.st_rowptr) : out->row_ptr;
+  uint32_t* col_dev = host ? (uint32_t*)(ws + Lw.st_edges) : out->col;
+  uint32_t* pairs_dev = host ? (uint32_t*)(ws + Lw.st_edges) : out->pairs;
+  // device-mode callers may keep the sampled points directly
+  if (sample && !host) {
+    if (out->theta_out) theta = out->theta_out;
+    if (out->r_out) r = out->r_out;
+  }
+
+  Timer tm;
+  tm.init(out->timing != nullptr, st);
+  int launches = 0;
+  tm.mark();  // 0
+  CK(cudaMemsetAsync(hist, 0, 4 * kMaxBands, st));
+  CK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), st));
+  float ms_h2d = 0;
+  if (sample) {
+    CK(launch_sample(n, seed, alpha, R, bc, theta, r, keys_a, vals_a, hist, st));
+    ++launches;
+  } else {
+    const double* th_src = theta_in;
+    const double* r_src = r_in;
+    if (host) {
+      CK(cudaMemcpyAsync(theta, theta_in, 8 * n, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(r, r_in, 8 * n, cudaMemcpyHostToDevice, st));
+      th_src = theta;
+      r_src = r;
+    } else {
+      theta = const_cast<double*>(theta_in);
+      r = const_cast<double*>(r_in);
+    }
+    CK(launch_keys_from_points(n, th_src, r_src, bc, keys_a, vals_a, hist, sc, st));
+    ++launches;
+  }
+  CK(launch_band_layout(bc, hist, lay, st));
+  ++launches;
+  tm.mark();  // 1
+  CK(radix_sort((uint32_t)n, keys_a, vals_a, keys_b, vals_b, ws + Lw.sort_tmp, 0, 32, st,
+                &launches));
+  tm.mark();  // 2
+  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, dir, st,
+                        &launches));
+  tm.mark();  // 3
+
+  QueryArgs qa{};
+  qa.n = (uint32_t)n;
+  qa.pts = pts;
+  qa.skey = keys_a;
+  qa.sid = vals_a;
+  qa.dir = dir;
+  qa.lay = lay;
+  qa.order = nullptr;
+  qa.deg = deg;
+  qa.sc = sc;
+  CK(launch_query(QM_COUNT, f, qa, bc, st));
+  ++launches;
+  tm.mark();  // 4
+  uint64_t* offs = (f == RHG_CSR) ? row_ptr_dev : offs_ws;
+  CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
+  tm.mark();  // 5
+  CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const DevScalars hs = *pin;
+  if (hs.domain_error) return RHG_ERR_DOMAIN;
+  *out->num_edges = hs.total;
+  if (out->R_used) *out->R_used = R;
+  if (hs.total > out->capacity_edges) return RHG_ERR_CAPACITY;
+  qa.offs = offs;
+  qa.col = col_dev;
+  qa.pairs = pairs_dev;
+  CK(launch_query(QM_EMIT, f, qa, bc, st));
+  ++launches;
+  tm.mark();  // 6
+  if (host) {
+    if (f == RHG_CSR) {
+      CK(cudaMemcpyAsync(out->row_ptr, row_ptr_dev, 8 * (n + 1), cudaMemcpyDeviceToHost, st));
+      if (hs.total)
+        CK(cudaMemcpyAsync(out->col, col_dev, 4 * hs.total, cudaMemcpyDeviceToHost, st));
+    } else if (hs.total) {
+      CK(cudaMemcpyAsync(out->pairs, pairs_dev, 8 * hs.total, cudaMemcpyDeviceToHost, st));
+    }
+    if (sample && out->theta_out)
+      CK(cudaMemcpyAsync(out->theta_out, theta, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (sample && out->r_out)
+      CK(cudaMemcpyAsync(out->r_out, r, 8 * n, cudaMemcpyDeviceToHost, st));
+  }
+  tm.mark();  // 7
+  if (host || out->timing) CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (out->timing) {
+    rhg_timing* t = out->timing;
+    t->ms_sample = tm.between(0, 1);
+    t->ms_sort = tm.between(1, 2);
+    t->ms_index = tm.between(2, 3);
+    t->ms_count = tm.between(3, 4);
+    t->ms_scan = tm.between(4, 5);
+    t->ms_emit = tm.between(5, 6);
+    t->ms_copy = tm.between(6, 7) + ms_h2d;
+    t->ms_total = tm.between(0, 7);
+    t->candidates = hs.candidates;
+    t->launches = (uint64_t)launches;
+    t->emit_retested = 1;
+  }
+  return RHG_OK;
+}
+
+}  // namespace
+
+#define RHG_EXPORT __attribute__((visibility("default")))
+
+extern "C" {
+
+RHG_EXPORT rhg_status rhg_target_radius(uint64_t n, double kbar, double gamma, double* R) {
+  if (!R || !(gamma > 2.0) || !std::isfinite(gamma) || n < 2) return RHG_ERR_INVALID;
+  return target_radius((double)n, kbar, (gamma - 1.0) / 2.0, R);
+}
+
+RHG_EXPORT rhg_status rhg_band_boundaries(uint64_t n, double R, const rhg_options* opt, int* L, double* c) {
+  if (!L || !c || n < 2 || !(R >= 0.0) || !std::isfinite(R)) return RHG_ERR_INVALID;
+  BandConst bc;
+  rhg_status s = make_band_const(n, R, opt, &bc);
+  if (s != RHG_OK) return s;
+  *L = bc.L;
+  for (int j = 0; j <= bc.L; ++j) c[j] = bc.c[j];
+  return RHG_OK;
+}
+
+RHG_EXPORT size_t rhg_workspace_bytes(uint64_t n, rhg_format format, uint64_t capacity_edges,
+                           int host_buffers) {
+  return plan_layout(n, format, capacity_edges, host_buffers ? 1 : 0).total;
+}
+
+RHG_EXPORT rhg_status rhg_generate_with_radius(uint64_t n, double R, double alpha, uint64_t seed,
+                                    const rhg_output* out, rhg_stream stream) {
+  if (!(alpha > 0.5) || !std::isfinite(alpha)) return RHG_ERR_INVALID;
+  return run(n, true, alpha, seed, nullptr, nullptr, R, out, (cudaStream_t)stream);
+}
+
+RHG_EXPORT rhg_status rhg_generate(uint64_t n, double kbar, double gamma, uint64_t seed,
+                        const rhg_output* out, rhg_stream stream) {
+  double R = 0.0;
+  rhg_status s = rhg_target_radius(n, kbar, gamma, &R);
+  if (s != RHG_OK) return s;
+  return rhg_generate_with_radius(n, R, (gamma - 1.0) / 2.0, seed, out, stream);
+}
+
+RHG_EXPORT rhg_status rhg_generate_from_points(uint64_t n, const double* theta, const double* r, double R,
+                                    const rhg_output* out, rhg_stream stream) {
+  return run(n, false, 0.0, 0, theta, r, R, out, (cudaStream_t)stream);
+}
+
+RHG_EXPORT rhg_status rhg_sample_points(uint64_t n, double alpha, double R, uint64_t seed, double* theta,
+                             double* r, rhg_stream stream) {
+  if (n == 0 || !theta || !r || !(alpha > 0.5) || !(R >= 0.0) || !std::isfinite(std::cosh(alpha * R)))
+    return RHG_ERR_INVALID;
+  BandConst bc;
+  rhg_status s = make_band_const(n < 2 ? 2 : n, R, nullptr, &bc);
+  if (s != RHG_OK) return s;
+  CK(launch_sample(n, seed, alpha, R, bc, theta, r, nullptr, nullptr, nullptr,
+                   (cudaStream_t)stream));
+  return RHG_OK;
+}
+
+RHG_EXPORT rhg_status rhg_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out,
+                            rhg_stream stream) {
+  if (!out) return RHG_ERR_INVALID;
+  if (count == 0) return RHG_OK;
+  CK(launch_philox_words(seed, i0, count, out, (cudaStream_t)stream));
+  return RHG_OK;
+}
+
+RHG_EXPORT const char* rhg_status_string(rhg_status s) {
+  switch (s) {
+    case RHG_OK: return "ok";
+    case RHG_ERR_INVALID: return "invalid argument";
+    case RHG_ERR_CALIBRATION: return "calibration failed: kbar cannot be reached by Eq. 22";
+    case RHG_ERR_WORKSPACE: return "workspace too small";
+    case RHG_ERR_CAPACITY: return "output capacity too small (required count in *num_edges)";
+    case RHG_ERR_DOMAIN: return "input point outside the disk";
+    case RHG_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+RHG_EXPORT const char* rhg_version(void) { return RHG_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Exact edge-set equality is required except for pairs the oracle
+flags as near-ties (|cosh d - cosh R| <= 1e-12 cosh R), which are counted and
+reported (expected 0).  Run with -m gpu on a B200."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {  # BASELINE.json configs (n, kbar, gamma, seed)
+    1: (10_000, 6, 3.0, 1),
+    2: (1_000_000, 10, 3.0, 2),
+    3: (10_000_000, 100, 3.0, 3),
+    4: (1_000_000, 32, 2.2, 4),
+    5: (100_000_000, 16, 2.7, 5),
+}
+
+
+@pytest.fixture(scope="module")
+def rhg():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1606_09481_b200 as rhg
+    rhg.lib()  # in-tree librhg.so, loud failure if missing
+    return rhg
+
+
+def keys_of(p):
+    p = np.asarray(p, dtype=np.uint64).reshape(-1, 2)
+    return (p[:, 0] << np.uint64(32)) | p[:, 1]
+
+
+def csr_checked_pairs(g):
+    """Canonical (u < v) pairs from the GPU CSR, after checking symmetry and no
+    self-loops on the full directed list."""
+    rp = g.row_ptr.cpu().numpy()
+    col = g.col.cpu().numpy().view(np.uint32).astype(np.uint64)
+    n = len(rp) - 1
+    assert rp[0] == 0 and np.all(np.diff(rp) >= 0) and rp[-1] == len(col)
+    u = np.repeat(np.arange(n, dtype=np.uint64), np.diff(rp).astype(np.int64))
+    assert not np.any(u == col), "self-loop"
+    assert np.all(col < n)
+    fwd = np.sort((u << np.uint64(32)) | col)
+    bwd = np.sort((col << np.uint64(32)) | u)
+    assert np.array_equal(fwd, bwd), "CSR not symmetric"
+    assert len(np.unique(fwd)) == len(fwd), "duplicate entries"
+    keep = u < col
+    return np.sort((u[keep] << np.uint64(32)) | col[keep])
+
+
+def pairs_checked(g):
+    p = g.pairs.cpu().numpy().view(np.uint32).astype(np.uint64)
+    assert np.all(p[:, 0] < p[:, 1])
+    k = np.sort((p[:, 0] << np.uint64(32)) | p[:, 1])
+    assert len(np.unique(k)) == len(k), "duplicate undirected edge"
+    return k
+
+
+def compare_sets(gpu_keys, es):
+    """Exact equality except oracle-flagged near ties; returns #excused."""
+    ref = np.sort(keys_of(es.pairs))
+    only_gpu = np.setdiff1d(gpu_keys, ref, assume_unique=True)
+    only_ref = np.setdiff1d(ref, gpu_keys, assume_unique=True)
+    ties = set(keys_of(es.ties).tolist())
+    bad = [k for k in np.concatenate([only_gpu, only_ref]).tolist() if k not in ties]
+    assert not bad, f"{len(bad)} non-tie disagreements, e.g. {[(k >> 32, k & 0xffffffff) for k in bad[:5]]}"
+    return len(only_gpu) + len(only_ref)
+
+
+def oracle_points(orc, n, kbar, gamma, seed):
+    a = orc.alpha(gamma)
+    R = orc.target_radius(n, kbar, a)
+    th, r = orc.sample_points(n, a, R, seed)
+    return th, r, R, a
+
+
+# --------------------------------------------------------------------------- sampler
+@pytest.mark.parametrize("seed,i0", [(1, 0), (3, 12345), (0xDEADBEEFCAFEF00D, 2**32 - 100)])
+def test_philox_words_bit_exact(rhg, orc, seed, i0):
+    w = rhg.philox_words(seed, i0, 50_000).cpu().numpy().view(np.uint32)
+    assert np.array_equal(w, orc.philox_words(seed, i0, 50_000))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_sampler_matches_oracle(rhg, orc, cfg):
+    """theta bit-exact (same IEEE ops); r within 8 ulp (device vs glibc asinh)."""
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    th_o, r_o, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    th, r = rhg.sample_points(n, a, R, seed)
+    th, r = th.cpu().numpy(), r.cpu().numpy()
+    assert np.array_equal(th, th_o)
+    ulp = np.spacing(np.maximum(r_o, 1e-300))
+    assert np.all(np.abs(r - r_o) <= 8 * ulp)
+    assert r.max() <= R and r.min() >= 0
+
+
+# --------------------------------------------------------------------------- edge sets
+@pytest.mark.parametrize("cfg,fmt", [(1, "csr"), (1, "pairs"), (2, "csr"), (2, "pairs"),
+                                     (4, "csr"), (4, "pairs")])
+def test_edges_from_oracle_points(rhg, orc, cfg, fmt):
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    es = orc.brute_force(th, r, R) if n <= 20_000 else orc.sweep(th, r, R)
+    g = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R, fmt)
+    gk = csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g)
+    excused = compare_sets(gk, es)
+    print(f"cfg{cfg} {fmt}: m={es.m} ties={len(es.ties)} excused={excused}")
+
+
+@pytest.mark.parametrize("fmt", ["csr", "pairs"])
+def test_generate_equals_from_points_on_own_points(rhg, fmt):
+    """rhg_generate == rhg_generate_from_points on the points it sampled."""
+    n, kbar, gamma, seed = CONFIGS[2]
+    g = rhg.generate(n, kbar, gamma, seed, fmt, return_points=True)
+    g2 = rhg.generate_from_points(g.theta, g.r, g.R, fmt)
+    if fmt == "csr":
+        assert torch.equal(g.row_ptr, g2.row_ptr) and torch.equal(g.col, g2.col)
+    else:
+        assert torch.equal(g.pairs, g2.pairs)
+
+
+def test_deterministic(rhg):
+    n, kbar, gamma, seed = CONFIGS[4]
+    g1 = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True)
+    g2 = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True)
+    assert torch.equal(g1.theta, g2.theta) and torch.equal(g1.r, g2.r)
+    assert torch.equal(g1.row_ptr, g2.row_ptr) and torch.equal(g1.col, g2.col)
+
+
+@pytest.mark.parametrize("opts", [dict(num_bands=1), dict(num_bands=5, band_ratio=0.5),
+                                  dict(num_bands=32, band_ratio=0.97), dict(num_bands=20)])
+def test_edge_set_invariant_under_slab_layout(rhg, orc, opts):
+    """The slab layout (L, p) is a tuning knob: same edge set."""
+    n, kbar, gamma, seed = 20_000, 12, 2.4, 17
+    th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    es = orc.brute_force(th, r, R)
+    g = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R,
+                                 "csr", options=opts)
+    compare_sets(csr_checked_pairs(g), es)
+    g = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R,
+                                 "pairs", options=opts)
+    compare_sets(pairs_checked(g), es)
+
+
+# --------------------------------------------------------------------------- edge cases
+def _cpu_pts(th, r):
+    return torch.tensor(th, dtype=torch.float64).cuda(), torch.tensor(r, dtype=torch.float64).cuda()
+
+
+def test_edge_cases(rhg, orc):
+    rng = np.random.default_rng(3)
+    cases = []
+    # two points, one edge / no edge
+    cases.append(([0.1, 0.2], [5.0, 5.0], 10.0))
+    cases.append(([0.1, 3.0], [9.9, 9.9], 10.0))
+    # complete graph (every r1 + r2 < R), empty graph (R = 0 with distinct points)
+    cases.append((rng.uniform(0, 2 * np.pi, 50), rng.uniform(0, 40, 50), 90.0))
+    cases.append((rng.uniform(0, 2 * np.pi, 50), rng.uniform(0, 1e-3, 50) * 0, 0.0))
+    # duplicates, r = 0 and r = R, theta = 0 and just below 2pi, seam clusters
+    th = np.concatenate([np.zeros(5), np.full(5, np.nextafter(2 * np.pi, 0)), rng.uniform(0, 1e-7, 20),
+                         2 * np.pi - rng.uniform(1e-9, 1e-7, 20), rng.uniform(0, 2 * np.pi, 200)])
+    rr = np.concatenate([np.zeros(3), np.full(7, 12.0), rng.uniform(11, 12, 40),
+                         12.0 - rng.exponential(1.0, 200).clip(0, 12)])
+    cases.append((th, rr, 12.0))
+    # all points at one angle (huge buckets), many slabs for few points
+    cases.append((np.full(300, 1.234), rng.uniform(0, 15, 300), 15.0))
+    for th, r, R in cases:
+        th = np.asarray(th, dtype=np.float64)
+        r = np.asarray(r, dtype=np.float64)
+        es = orc.brute_force(th, r, R)
+        for fmt in ("csr", "pairs"):
+            g = rhg.generate_from_points(*_cpu_pts(th, r), R, fmt)
+            k = csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g)
+            compare_sets(k, es)
+    # complete graph check explicitly
+    th, r, R = cases[2]
+    g = rhg.generate_from_points(*_cpu_pts(th, r), R, "pairs")
+    assert g.num_edges == 50 * 49 // 2
+    th, r, R = cases[3]
+    assert rhg.generate_from_points(*_cpu_pts(th, r), R, "csr").num_edges == 50 * 49  # all coincide
+
+
+def test_ragged_sizes(rhg, orc):
+    """Sizes that are not multiples of warps / tiles / sort blocks."""
+    for n in (2, 3, 31, 33, 4095, 4097, 8193):
+        R = 2 * np.log(n) + 2.0
+        th, r = orc.sample_points(n, 0.8, R, n)
+        es = orc.brute_force(th, r, R)
+        g = rhg.generate_from_points(*_cpu_pts(th, r), R, "csr")
+        compare_sets(csr_checked_pairs(g), es)
+
+
+def test_domain_errors(rhg):
+    th = torch.tensor([0.1, 0.2, 0.3], dtype=torch.float64).cuda()
+    for bad_r in ([1.0, 2.0, 10.5], [1.0, -1e-9, 2.0], [1.0, float("nan"), 2.0]):
+        with pytest.raises(rhg.RhgError) as ei:
+            rhg.generate_from_points(th, torch.tensor(bad_r, dtype=torch.float64).cuda(), 10.0)
+        assert ei.value.status == rhg.RHG_ERR_DOMAIN
+    r = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64).cuda()
+    th2 = torch.tensor([0.1, 2 * np.pi, 0.3], dtype=torch.float64).cuda()
+    with pytest.raises(rhg.RhgError) as ei:
+        rhg.generate_from_points(th2, r, 10.0)
+    assert ei.value.status == rhg.RHG_ERR_DOMAIN
+
+
+def test_capacity_protocol(rhg):
+    n, kbar, gamma, seed = CONFIGS[1]
+    with pytest.raises(rhg.RhgError) as ei:
+        rhg.generate(n, kbar, gamma, seed, "csr", capacity=100)
+    assert ei.value.status == rhg.RHG_ERR_CAPACITY
+    g = rhg.generate(n, kbar, gamma, seed, "csr")
+    g2 = rhg.generate(n, kbar, gamma, seed, "csr", capacity=g.num_edges)
+    assert torch.equal(g.col, g2.col)
+
+
+def test_host_buffers_mode(rhg, orc):
+    n, kbar, gamma, seed = CONFIGS[1]
+    th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    g = rhg.generate_from_points(torch.from_numpy(th), torch.from_numpy(r), R, "csr")
+    assert not g.row_ptr.is_cuda
+    gd = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R, "csr")
+    assert torch.equal(g.row_ptr, gd.row_ptr.cpu()) and torch.equal(g.col, gd.col.cpu())
+    gh = rhg.generate(n, kbar, gamma, seed, "pairs", host_buffers=True, return_points=True)
+    gg = rhg.generate(n, kbar, gamma, seed, "pairs", return_points=True)
+    assert torch.equal(gh.pairs, gg.pairs.cpu()) and torch.equal(gh.theta, gg.theta.cpu())
+
+
+# --------------------------------------------------------------------------- full sizes
+def _sampled_rows_check(rhg_graph_rows, orc, th, r, R, queries):
+    off, nbr, ntie = orc.rows(th, r, R, queries)
+    excused = 0
+    for k, v in enumerate(queries):
+        ref = nbr[off[k]:off[k + 1]]
+        got = rhg_graph_rows(int(v))
+        if not np.array_equal(np.sort(got), ref):
+            diff = np.setxor1d(got, ref)
+            w, _ = orc.row_ties(th, r, R, int(v))
+            assert set(diff.tolist()) <= set(w.tolist()), f"vertex {v}: {diff[:10]}"
+            excused += len(diff)
+    return excused
+
+
+@pytest.mark.parametrize("cfg", [3])
+def test_full_size_csr_sampled_rows(rhg, orc, cfg):
+    """BASELINE config 3 in the bench's launch configuration (rhg_generate, CSR):
+    points vs the oracle's sampler, then 48 sampled rows vs oracle brute force
+    over all 1e7 points, plus symmetry of those rows."""
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    th_o, r_o, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    g = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True)
+    assert g.R == pytest.approx(R, rel=1e-13)
+    th, r = g.theta.cpu().numpy(), g.r.cpu().numpy()
+    assert np.array_equal(th, th_o)
+    assert np.all(np.abs(r - r_o) <= 8 * np.spacing(np.maximum(r_o, 1e-300)))
+    rp = g.row_ptr.cpu().numpy()
+    assert rp[-1] == g.num_edges
+    rng = np.random.default_rng(cfg)
+    q = np.concatenate([rng.choice(n, 40, replace=False), np.argsort(r_o)[:8]]).astype(np.uint32)
+    col = g.col
+    rows = lambda v: col[rp[v]:rp[v + 1]].cpu().numpy().view(np.uint32)
+    _sampled_rows_check(rows, orc, th_o, r_o, R, q)
+    for v in q[:10]:
+        for w in rows(int(v))[:50]:
+            assert int(v) in set(rows(int(w)).tolist())
+    mean = g.num_edges / n
+    assert abs(mean - kbar) / kbar < 0.03
+
+
+def test_full_size_pairs_sampled_degrees(rhg, orc):
+    """BASELINE config 5 (n = 1e8, undirected uint32 list): neighbourhoods of 12
+    sampled vertices vs oracle brute force over all points."""
+    n, kbar, gamma, seed = CONFIGS[5]
+    th_o, r_o, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    g = rhg.generate(n, kbar, gamma, seed, "pairs", return_points=True)
+    assert torch.equal(g.theta.cpu(), torch.from_numpy(th_o))
+    P = g.pairs
+    rng = np.random.default_rng(5)
+    q = np.concatenate([rng.choice(n, 8, replace=False), np.argsort(r_o)[:4]]).astype(np.uint32)
+
+    def row(v):
+        v32 = torch.tensor(int(v), dtype=torch.int64, device=P.device)
+        pu = P[:, 0].to(torch.int64) & 0xffffffff
+        pv = P[:, 1].to(torch.int64) & 0xffffffff
+        a_ = pv[pu == v32]
+        b_ = pu[pv == v32]
+        return torch.cat([a_, b_]).cpu().numpy().astype(np.uint32)
+
+    _sampled_rows_check(row, orc, th_o, r_o, R, q)
+    mean = 2 * g.num_edges / n
+    assert abs(mean - kbar) / kbar < 0.03
