@@ -77,7 +77,8 @@ typedef struct {
   float ms_emit;     /* K8: edge emission                                       */
   float ms_copy;     /* host-buffer mode: device <-> host copies                */
   float ms_total;    /* first to last event                                     */
-  uint64_t candidates;     /* candidate (vertex, point) tests performed in the count pass */
+  uint64_t candidates;     /* candidate (vertex, point) pairs tested exactly in the count pass */
+  uint64_t certain;        /* edges accepted by the certified inner window, without a test */
   uint64_t launches;       /* kernels launched by this call                                 */
   uint64_t emit_retested;  /* 1 if the emit pass had to re-run the tests (bit buffer overflow) */
 } rhg_timing;
@@ -119,7 +120,7 @@ rhg_status rhg_band_boundaries(uint64_t n, double R, const rhg_options *opt, int
    proves too small at run time the emit pass re-runs the tests instead
    (slower, same output). */
 size_t rhg_workspace_bytes(uint64_t n, rhg_format format, uint64_t capacity_edges,
-                           int host_buffers);
+                           int host_buffers, const rhg_options *options);
 
 /* Algorithm 1 end to end: alpha from gamma (line 1), R from
    getTargetRadius (line 2), then on `stream`: Philox point sampling (lines 7-8;

@@ -47,7 +47,8 @@ class Timing(ctypes.Structure):
                 ("ms_index", ctypes.c_float), ("ms_count", ctypes.c_float),
                 ("ms_scan", ctypes.c_float), ("ms_emit", ctypes.c_float),
                 ("ms_copy", ctypes.c_float), ("ms_total", ctypes.c_float),
-                ("candidates", ctypes.c_uint64), ("launches", ctypes.c_uint64),
+                ("candidates", ctypes.c_uint64), ("certain", ctypes.c_uint64),
+                ("launches", ctypes.c_uint64),
                 ("emit_retested", ctypes.c_uint64)]
 
     def as_dict(self):
@@ -83,7 +84,8 @@ def lib() -> ctypes.CDLL:
         L.rhg_band_boundaries.argtypes = [u64, f64, ctypes.POINTER(Options),
                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(f64)]
         L.rhg_workspace_bytes.restype = ctypes.c_size_t
-        L.rhg_workspace_bytes.argtypes = [u64, ctypes.c_int, u64, ctypes.c_int]
+        L.rhg_workspace_bytes.argtypes = [u64, ctypes.c_int, u64, ctypes.c_int,
+                                          ctypes.POINTER(Options)]
         L.rhg_generate.restype = st
         L.rhg_generate.argtypes = [u64, f64, f64, u64, ctypes.POINTER(Output), vp]
         L.rhg_generate_with_radius.restype = st
@@ -138,8 +140,17 @@ def band_boundaries(n: int, R: float, num_bands: int = 0, band_ratio: float = 0.
     return np.array(c[: L.value + 1])
 
 
-def workspace_bytes(n: int, fmt: str = "csr", capacity: int = 0, host_buffers: bool = False) -> int:
-    return int(lib().rhg_workspace_bytes(n, FORMATS[fmt], capacity, int(host_buffers)))
+def workspace_bytes(n: int, fmt: str = "csr", capacity: int = 0, host_buffers: bool = False,
+                    options=None) -> int:
+    o = None if options is None else ctypes.byref(_options(options))
+    return int(lib().rhg_workspace_bytes(n, FORMATS[fmt], capacity, int(host_buffers), o))
+
+
+def _options(options) -> Options:
+    if options is None:
+        return Options(0, 0.0, 0)
+    return Options(int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
+                   int(options.get("heavy_threshold", 0)))
 
 
 def version() -> str:
@@ -194,12 +205,10 @@ def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspac
     f = FORMATS[fmt]
     fmt = "csr" if f == RHG_CSR else "pairs"
     cap = int(capacity) if capacity is not None else _expected_capacity(n, kbar_hint, fmt)
-    opts = Options(0, 0.0, 0) if options is None else Options(
-        int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
-        int(options.get("heavy_threshold", 0)))
+    opts = _options(options)
     ws = workspace if workspace is not None else Workspace(device)
     for attempt in range(2):
-        nbytes = int(lib().rhg_workspace_bytes(n, f, cap, int(host_buffers)))
+        nbytes = int(lib().rhg_workspace_bytes(n, f, cap, int(host_buffers), ctypes.byref(opts)))
         wbuf = ws.get(nbytes)
         if out_bufs is not None:
             row_ptr, col, pairs, theta, r = out_bufs(cap)

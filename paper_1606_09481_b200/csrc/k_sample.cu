@@ -117,13 +117,22 @@ __global__ void __launch_bounds__(256)
 }
 
 // One warp: band offsets, bucket-directory geometry.  Buckets per band: the
-// power of two >= ceil(n_j / 2) (about 1-2 points per bucket), capped at 2^27.
-__global__ void k_band_layout(int L, const uint32_t* __restrict__ band_hist, BandLayout* lay) {
+// power of two >= 4 n_j (1/8 .. 1/4 point per bucket), capped at 2^27.
+// Hub split: E_j = sum_k n_k min(1, dphi(c_j, c_k)/pi) bounds the expected
+// candidate count of a vertex in band j (its radius is >= c_j and windows shrink
+// with radius); bands with E_j above the
+// threshold form the hub prefix [0, heavy_end) of the sorted order.
+__global__ void k_band_layout(const __grid_constant__ BandConst bc,
+                              const uint32_t* __restrict__ band_hist, BandLayout* lay,
+                              HeavyMeta* meta) {
+  const int L = bc.L;
   int j = threadIdx.x;
   uint32_t cnt = (j < L) ? band_hist[j] : 0u;
   uint32_t nb = 1, sh = kQBits;
   if (j < L) {
-    uint32_t want = (cnt + 1) / 2;
+    // >= 4 buckets per point: range ends are whole buckets (no key probing in the
+    // queries), so fine buckets keep the boundary-bucket overhead small
+    uint32_t want = cnt > (1u << 25) ? (1u << 27) : 4u * cnt;
     while (nb < want && sh > 0) {
       nb <<= 1;
       --sh;
@@ -141,16 +150,45 @@ __global__ void k_band_layout(int L, const uint32_t* __restrict__ band_hist, Ban
       s_dir += b;
     }
   }
+  // expected candidates of a vertex sitting on band j's inner boundary
+  double E = 0.0;
+  if (j < L) {
+    for (int k = 0; k < L; ++k) {
+      double nk = (double)band_hist[k];
+      if (nk == 0.0) continue;
+      double frac = 1.0;
+      if (bc.invS[j] != 0.0 && bc.invS[k] != 0.0) {
+        double h = bc.A[j] * bc.B[k] - bc.B[j] * bc.A[k];
+        double ratio = (bc.T4 - h * h) * (0.25 * bc.invS[j]) * bc.invS[k];
+        if (ratio < 1.0) frac = 2.0 * asin(sqrt(fmax(ratio, 0.0))) / 3.141592653589793;
+      }
+      E += nk * frac;
+    }
+  }
+  bool heavy = (j < L) && (E > bc.heavy_threshold);
+  uint32_t hmask = __ballot_sync(0xffffffffu, heavy);
+  // bands are ordered inner -> outer and E_j is non-increasing: hubs = prefix
+  int J = __ffs(~hmask) - 1;  // first light band
+  if (J < 0 || J > L) J = L;
+  uint32_t startJ = __shfl_sync(0xffffffffu, s_cnt - cnt, J < 32 ? J : 31);
+  uint32_t total = __shfl_sync(0xffffffffu, s_cnt, 31);
+  if (J >= L) startJ = total;
   if (j < L) {
     lay->count[j] = cnt;
     lay->start[j] = s_cnt - cnt;
     lay->dir_off[j] = s_dir - dsz;
     lay->shift[j] = sh;
     lay->nb[j] = nb;
+    lay->expected[j] = (float)E;
   }
   if (j == L - 1) {
     lay->start[L] = s_cnt;
     lay->dir_off[L] = s_dir;
+  }
+  if (j == 0) {
+    uint32_t he = startJ < bc.heavy_cap ? startJ : bc.heavy_cap;
+    lay->heavy_end = he;
+    meta->nslots = (unsigned long long)he * kRangesPerSlab * (unsigned long long)L;
   }
 }
 
@@ -184,8 +222,8 @@ cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const doubl
 }
 
 cudaError_t launch_band_layout(const BandConst& bc, const uint32_t* band_hist, BandLayout* lay,
-                               cudaStream_t st) {
-  k_band_layout<<<1, 32, 0, st>>>(bc.L, band_hist, lay);
+                               HeavyMeta* meta, cudaStream_t st) {
+  k_band_layout<<<1, 32, 0, st>>>(bc, band_hist, lay, meta);
   return cudaGetLastError();
 }
 

@@ -119,10 +119,18 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
   return res;
 }
 
+__device__ __forceinline__ uint64_t dev_count(uint64_t n, const unsigned long long* n_dev) {
+  if (!n_dev) return n;
+  uint64_t d = *n_dev;
+  return d < n ? d : n;
+}
+
 template <typename TIn, typename TAcc>
 __global__ void __launch_bounds__(SC_THREADS)
-    k_scan_reduce(uint64_t n, const TIn* __restrict__ in, TAcc* __restrict__ partial) {
+    k_scan_reduce(uint64_t n, const TIn* __restrict__ in, TAcc* __restrict__ partial,
+                  const unsigned long long* n_dev) {
   __shared__ TAcc sh[33];
+  n = dev_count(n, n_dev);
   uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK;
   TAcc s = 0;
 #pragma unroll
@@ -136,9 +144,10 @@ __global__ void __launch_bounds__(SC_THREADS)
 }
 
 // single block: exclusive scan of the partials in place; total -> *total
-template <typename TAcc>
+template <typename TAcc, typename TOut>
 __global__ void __launch_bounds__(SC_THREADS)
-    k_scan_partials(uint32_t m, TAcc* partial, TAcc* total_slot, unsigned long long* total_out) {
+    k_scan_partials(uint32_t m, TAcc* partial, TOut* out_base, uint64_t n,
+                    const unsigned long long* n_dev, unsigned long long* total_out) {
   __shared__ TAcc sh[33];
   TAcc carry = 0;
   for (uint32_t base = 0; base < m; base += SC_THREADS) {
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(SC_THREADS)
     carry += tot;
   }
   if (threadIdx.x == 0) {
-    if (total_slot) *total_slot = carry;
+    if (out_base) out_base[dev_count(n, n_dev)] = (TOut)carry;
     if (total_out) *total_out = (unsigned long long)carry;
   }
 }
@@ -159,8 +168,10 @@ __global__ void __launch_bounds__(SC_THREADS)
 template <typename TIn, typename TOut, typename TAcc>
 __global__ void __launch_bounds__(SC_THREADS)
     k_scan_down(uint64_t n, const TIn* __restrict__ in, TOut* __restrict__ out,
-                const TAcc* __restrict__ partial) {
+                const TAcc* __restrict__ partial, const unsigned long long* n_dev) {
   __shared__ TAcc sh[33];
+  n = dev_count(n, n_dev);
+  if ((uint64_t)blockIdx.x * SC_CHUNK >= n) return;
   uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK + (uint64_t)threadIdx.x * SC_ITEMS;
   TAcc v[SC_ITEMS];
   TAcc s = 0;
@@ -185,12 +196,21 @@ size_t scan_tmp_bytes(uint64_t n) { return (size_t)(sc_blocks(n) + 2) * sizeof(u
 
 cudaError_t exclusive_scan_u32_u64(uint32_t n, const uint32_t* in, uint64_t* out, void* tmp,
                                    unsigned long long* total_out, cudaStream_t st, int* launches) {
-  uint32_t B = sc_blocks(n);
+  return exclusive_scan_u32_u64_dev(n, nullptr, in, out, tmp, total_out, st, launches);
+}
+
+cudaError_t exclusive_scan_u32_u64_dev(uint64_t n_cap, const unsigned long long* n_dev,
+                                       const uint32_t* in, uint64_t* out, void* tmp,
+                                       unsigned long long* total_out, cudaStream_t st,
+                                       int* launches) {
+  uint32_t B = sc_blocks(n_cap);
   if (B == 0) B = 1;
   uint64_t* partial = (uint64_t*)tmp;
-  k_scan_reduce<uint32_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n, in, partial);
-  k_scan_partials<uint64_t><<<1, SC_THREADS, 0, st>>>(B, partial, out + n, total_out);
-  k_scan_down<uint32_t, uint64_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n, in, out, partial);
+  k_scan_reduce<uint32_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n_cap, in, partial, n_dev);
+  k_scan_partials<uint64_t, uint64_t><<<1, SC_THREADS, 0, st>>>(B, partial, out, n_cap, n_dev,
+                                                                total_out);
+  k_scan_down<uint32_t, uint64_t, uint64_t><<<B, SC_THREADS, 0, st>>>(n_cap, in, out, partial,
+                                                                      n_dev);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
@@ -198,9 +218,11 @@ cudaError_t exclusive_scan_u32_u64(uint32_t n, const uint32_t* in, uint64_t* out
 static cudaError_t exclusive_scan_u32_inplace(uint32_t n, uint32_t* data, uint32_t* partial,
                                               cudaStream_t st, int* launches) {
   uint32_t B = sc_blocks(n);
-  k_scan_reduce<uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, partial);
-  k_scan_partials<uint32_t><<<1, SC_THREADS, 0, st>>>(B, partial, nullptr, nullptr);
-  k_scan_down<uint32_t, uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, data, partial);
+  k_scan_reduce<uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, partial, nullptr);
+  k_scan_partials<uint32_t, uint32_t><<<1, SC_THREADS, 0, st>>>(B, partial, (uint32_t*)nullptr, n,
+                                                                nullptr, nullptr);
+  k_scan_down<uint32_t, uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, data, partial,
+                                                                      nullptr);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }

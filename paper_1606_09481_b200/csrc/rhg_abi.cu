@@ -74,6 +74,11 @@ void make_boundaries(double R, int L, double p, double* c) {
   c[L] = R;
 }
 
+uint64_t heavy_cap_for(uint64_t n) {
+  uint64_t c = n / 128 + 4096;
+  return c < n ? c : n;
+}
+
 rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandConst* bc) {
   int L = (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
   double p = (opt && opt->band_ratio > 0.0) ? opt->band_ratio : 0.9;
@@ -84,11 +89,13 @@ rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandCon
   const double h = std::sinh(R / 2.0);
   bc->T4 = 4.0 * h * h;
   make_boundaries(R, L, p, bc->c);
-  for (int j = 0; j < L; ++j) {
+  for (int j = 0; j <= L; ++j) {
     bc->A[j] = std::exp(0.5 * bc->c[j]);
     bc->B[j] = std::exp(-0.5 * bc->c[j]);
     bc->invS[j] = bc->c[j] > 0.0 ? 1.0 / std::sinh(bc->c[j]) : 0.0;
   }
+  bc->heavy_threshold = (opt && opt->heavy_threshold) ? (double)opt->heavy_threshold : 1024.0;
+  bc->heavy_cap = (uint32_t)heavy_cap_for(n);
   return RHG_OK;
 }
 
@@ -98,10 +105,33 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, dir, deg, offs,
       scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
+  size_t h_start, h_len, h_lenw, h_soff, h_soffw, h_cc, h_choff, h_cslot, h_chits, h_cpos, h_meta,
+      h_bits;
+  size_t b_pool, b_next, b_first, b_cursor;
+  uint64_t nslots_cap, chunk_cap, hbits_cap, pool_blocks, pool_sub_blocks, light_warps;
 };
 
-Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host) {
+constexpr uint64_t kChunkExtra = 1ull << 21;
+constexpr uint64_t kChunkMin = 2048;
+
+int bands_for(uint64_t n, const rhg_options* opt) {
+  return (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
+}
+
+Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands) {
   Layout L{};
+  if (nbands < 1) nbands = 1;
+  if (nbands > kMaxBands) nbands = kMaxBands;
+  L.nslots_cap = heavy_cap_for(n) * (uint64_t)kRangesPerSlab * (uint64_t)nbands;
+  L.chunk_cap = L.nslots_cap + kChunkExtra;
+  // Candidate bits (emit replays them instead of re-testing).  Expected tests:
+  // ~1.14 per directed CSR entry, ~1.2 per undirected edge (outward scan); sized
+  // with margin from the output capacity.  Overflow falls back to re-testing.
+  const uint64_t cap_tests = (f == RHG_CSR) ? cap + cap / 2 : 2 * cap;
+  L.light_warps = (n + 31) / 32;
+  L.pool_sub_blocks = (cap_tests / 1024 + L.light_warps + 64 * 16) / kBitSubPools + 1;
+  L.pool_blocks = L.pool_sub_blocks * kBitSubPools;
+  L.hbits_cap = cap_tests / 64 + L.nslots_cap + 1024;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -118,10 +148,31 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host) {
   L.hist = take(4 * kMaxBands);
   L.lay = take(sizeof(BandLayout));
   L.pts = take(sizeof(PointRec) * n);
-  L.dir = take(4 * (n + 4 * kMaxBands + 8));
+  L.dir = take(4 * (8 * n + 4 * kMaxBands + 8));  // <= 8 n_j + 1 entries per band
   L.deg = take(4 * n);
   L.offs = take(8 * (n + 1));
-  L.scan_tmp = take(scan_tmp_bytes(n));
+  {
+    uint64_t m = n;
+    if (L.nslots_cap > m) m = L.nslots_cap;
+    if (L.chunk_cap > m) m = L.chunk_cap;
+    L.scan_tmp = take(scan_tmp_bytes(m));
+  }
+  L.h_start = take(4 * L.nslots_cap);
+  L.h_len = take(4 * L.nslots_cap);
+  L.h_lenw = take(4 * L.nslots_cap);
+  L.h_soff = take(8 * (L.nslots_cap + 1));
+  L.h_soffw = take(8 * (L.nslots_cap + 1));
+  L.h_bits = take(4 * L.hbits_cap);
+  L.b_pool = take(128 * L.pool_blocks);
+  L.b_next = take(4 * L.pool_blocks);
+  L.b_first = take(4 * L.light_warps);
+  L.b_cursor = take(4 * kBitSubPools);
+  L.h_cc = take(4 * L.nslots_cap);
+  L.h_choff = take(8 * (L.nslots_cap + 1));
+  L.h_cslot = take(4 * L.chunk_cap);
+  L.h_chits = take(4 * L.chunk_cap);
+  L.h_cpos = take(8 * (L.chunk_cap + 1));
+  L.h_meta = take(sizeof(HeavyMeta));
   L.sc = take(sizeof(DevScalars));
   L.st_rowptr = host && f == RHG_CSR ? take(8 * (n + 1)) : o;
   L.st_edges = host ? take(f == RHG_CSR ? 4 * cap : 8 * cap) : o;
@@ -200,7 +251,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   BandConst bc;
   rhg_status s = make_band_const(n, R, out->options, &bc);
   if (s != RHG_OK) return s;
-  const Layout Lw = plan_layout(n, f, out->capacity_edges, host);
+  const Layout Lw = plan_layout(n, f, out->capacity_edges, host, bc.L);
   if (!out->workspace || out->workspace_bytes < Lw.total) return RHG_ERR_WORKSPACE;
   DevScalars* pin = pinned_scalars();
   if (!pin) return RHG_ERR_CUDA;
@@ -253,7 +304,8 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     CK(launch_keys_from_points(n, th_src, r_src, bc, keys_a, vals_a, hist, sc, st));
     ++launches;
   }
-  CK(launch_band_layout(bc, hist, lay, st));
+  HeavyMeta* hmeta = (HeavyMeta*)(ws + Lw.h_meta);
+  CK(launch_band_layout(bc, hist, lay, hmeta, st));
   ++launches;
   tm.mark();  // 1
   CK(radix_sort((uint32_t)n, keys_a, vals_a, keys_b, vals_b, ws + Lw.sort_tmp, 0, 32, st,
@@ -271,8 +323,37 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.dir = dir;
   qa.lay = lay;
   qa.order = nullptr;
+  qa.bits = (uint32_t*)(ws + Lw.b_pool);
+  qa.bit_next = (uint32_t*)(ws + Lw.b_next);
+  qa.warp_first = (uint32_t*)(ws + Lw.b_first);
+  qa.pool_cursor = (uint32_t*)(ws + Lw.b_cursor);
+  qa.pool_sub_blocks = (uint32_t)Lw.pool_sub_blocks;
+  CK(cudaMemsetAsync(qa.pool_cursor, 0, 4 * kBitSubPools, st));
+  CK(cudaMemsetAsync(qa.warp_first, 0xff, 4 * Lw.light_warps, st));
   qa.deg = deg;
   qa.sc = sc;
+  HeavyArgs ha{};
+  ha.start = (uint32_t*)(ws + Lw.h_start);
+  ha.len = (uint32_t*)(ws + Lw.h_len);
+  ha.lenw = (uint32_t*)(ws + Lw.h_lenw);
+  ha.soff = (uint64_t*)(ws + Lw.h_soff);
+  ha.soffw = (uint64_t*)(ws + Lw.h_soffw);
+  ha.bits = (uint32_t*)(ws + Lw.h_bits);
+  ha.bits_cap = Lw.hbits_cap;
+  ha.cc = (uint32_t*)(ws + Lw.h_cc);
+  ha.choff = (uint64_t*)(ws + Lw.h_choff);
+  ha.chunk_slot = (uint32_t*)(ws + Lw.h_cslot);
+  ha.chunk_hits = (uint32_t*)(ws + Lw.h_chits);
+  ha.chunk_pos = (uint64_t*)(ws + Lw.h_cpos);
+  ha.meta = hmeta;
+  ha.nslots_cap = (uint64_t)bc.heavy_cap * kRangesPerSlab * (uint64_t)bc.L;
+  ha.chunk_cap = Lw.chunk_cap;
+  ha.chunk_min = kChunkMin;
+  CK(launch_heavy_plan(f, qa, ha, bc, ws + Lw.scan_tmp, st, &launches));
+  CK(launch_heavy(QM_COUNT, f, qa, ha, bc, st));
+  ++launches;
+  CK(exclusive_scan_u32_u64_dev(ha.chunk_cap, &hmeta->nchunks, ha.chunk_hits, ha.chunk_pos,
+                                ws + Lw.scan_tmp, &hmeta->hits, st, &launches));
   CK(launch_query(QM_COUNT, f, qa, bc, st));
   ++launches;
   tm.mark();  // 4
@@ -289,8 +370,11 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.offs = offs;
   qa.col = col_dev;
   qa.pairs = pairs_dev;
-  CK(launch_query(QM_EMIT, f, qa, bc, st));
-  ++launches;
+  // hub chunks replay their bits unless the hub bit buffer overflowed (checked on
+  // the device); light warps replay theirs unless a sub-pool ran dry.
+  CK(launch_heavy(QM_EMIT_BITS, f, qa, ha, bc, st));
+  CK(launch_query(hs.bit_overflow ? QM_EMIT : QM_EMIT_BITS, f, qa, bc, st));
+  launches += 2;
   tm.mark();  // 6
   if (host) {
     if (f == RHG_CSR) {
@@ -319,8 +403,9 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     t->ms_copy = tm.between(6, 7) + ms_h2d;
     t->ms_total = tm.between(0, 7);
     t->candidates = hs.candidates;
+    t->certain = hs.certain;
     t->launches = (uint64_t)launches;
-    t->emit_retested = 1;
+    t->emit_retested = hs.bit_overflow ? 1 : 0;
   }
   return RHG_OK;
 }
@@ -347,8 +432,8 @@ RHG_EXPORT rhg_status rhg_band_boundaries(uint64_t n, double R, const rhg_option
 }
 
 RHG_EXPORT size_t rhg_workspace_bytes(uint64_t n, rhg_format format, uint64_t capacity_edges,
-                           int host_buffers) {
-  return plan_layout(n, format, capacity_edges, host_buffers ? 1 : 0).total;
+                           int host_buffers, const rhg_options* options) {
+  return plan_layout(n, format, capacity_edges, host_buffers ? 1 : 0, bands_for(n, options)).total;
 }
 
 RHG_EXPORT rhg_status rhg_generate_with_radius(uint64_t n, double R, double alpha, uint64_t seed,

@@ -13,6 +13,8 @@ constexpr int kBandShift = 27;         // sort key = band << 27 | q27(theta)
 constexpr uint32_t kQBits = 27;
 constexpr uint32_t kQMax = (1u << kQBits) - 1u;
 constexpr uint32_t kQMask = kQMax;
+constexpr uint32_t kBitSubPools = 64;  // light-warp bit blocks come from 64 sub-pools
+constexpr uint32_t kRangesPerSlab = 7;  // per (vertex, slab): 4 pieces to test + 3 certain
 
 // fl(2*pi) and the remainder 2*pi - fl(2*pi): seam differences (Z13)
 #define RHG_TWO_PI_HI 0x1.921fb54442d18p+2
@@ -26,9 +28,11 @@ struct BandConst {
   double R;
   double T4;                 // 4 sinh^2(R/2) = 2 (cosh R - 1)       (Eq. 3 threshold, rewritten)
   double c[kMaxBands + 1];   // slab boundaries c_0 .. c_L
-  double A[kMaxBands];       // e^{c_j/2}
-  double B[kMaxBands];       // e^{-c_j/2}
-  double invS[kMaxBands];    // 1/sinh(c_j)   (0 for c_j = 0 -> full circle)
+  double A[kMaxBands + 1];   // e^{c_j/2}, j = 0..L
+  double B[kMaxBands + 1];   // e^{-c_j/2}
+  double invS[kMaxBands + 1];// 1/sinh(c_j)   (0 for c_j = 0 -> full circle)
+  double heavy_threshold;    // expected candidates per vertex above which a slab's vertices are hubs
+  uint32_t heavy_cap;        // at most this many hub vertices (workspace bound)
 };
 
 // Device-computed band layout after the band histogram.
@@ -38,12 +42,46 @@ struct BandLayout {
   uint32_t dir_off[kMaxBands + 1]; // offset of band j's bucket directory
   uint32_t shift[kMaxBands];       // bucket(q) = q >> shift[j]
   uint32_t nb[kMaxBands];          // buckets in band j (power of two)
+  uint32_t heavy_end;              // sorted positions [0, heavy_end) are hub vertices
+  float expected[kMaxBands];       // upper bound of E[candidates] for a vertex of band j
+};
+
+// Hub ("heavy") vertices: per (vertex, slab, wrap part) range slots, split into
+// fixed-size chunks that are spread over the whole GPU.
+struct HeavyMeta {
+  unsigned long long nslots;   // heavy_end * kRangesPerSlab * L
+  unsigned long long cand;     // total candidates in the slots
+  unsigned long long nchunks;  // total chunks
+  unsigned long long chunk;    // chunk size (candidates)
+  unsigned long long hits;     // total hits (directed / outward edges) of hub vertices
+  unsigned long long words;    // candidate-bit words of the hub slots
+  unsigned int bits_overflow;  // words > bits_cap: the hub emit re-tests
+};
+
+struct HeavyArgs {
+  uint32_t* start;          // [nslots_cap] first candidate (sorted position)
+  uint32_t* len;            // [nslots_cap] candidates in the slot
+  uint32_t* lenw;           // [nslots_cap] bit words of the slot (ceil(len/32))
+  uint64_t* soff;           // [nslots_cap + 1] scan of len
+  uint64_t* soffw;          // [nslots_cap + 1] scan of lenw
+  uint32_t* bits;           // [bits_cap] hub candidate bits
+  uint64_t bits_cap;
+  uint32_t* cc;             // [nslots_cap] chunks per slot
+  uint64_t* choff;          // [nslots_cap + 1] scan of cc
+  uint32_t* chunk_slot;     // [chunk_cap] slot of each chunk
+  uint32_t* chunk_hits;     // [chunk_cap]
+  uint64_t* chunk_pos;      // [chunk_cap + 1] scan of chunk_hits
+  HeavyMeta* meta;
+  uint64_t nslots_cap;
+  uint64_t chunk_cap;
+  uint64_t chunk_min;       // minimum chunk size
 };
 
 // Scalars the host reads back once per call.
 struct DevScalars {
   unsigned long long total;        // edges (directed for CSR, undirected for pairs)
   unsigned long long candidates;   // tests performed by the count pass
+  unsigned long long certain;      // edges accepted by the certified inner window (no test)
   unsigned long long bit_words;    // candidate-bit words allocated by the count pass
   unsigned int domain_error;       // a point outside the disk
   unsigned int bit_overflow;       // bit buffer too small -> emit re-tests
@@ -66,9 +104,11 @@ struct QueryArgs {
   const uint64_t* __restrict__ offs;  // emit pass: output offset per vertex id
   uint32_t* col;                      // CSR output
   uint32_t* pairs;                    // undirected output
-  uint32_t* bits;                     // candidate-bit buffer
-  uint64_t bits_cap;                  // words
-  uint64_t* warp_bits;                // per-warp bit base (count writes, emit reads)
+  uint32_t* bits;                     // light candidate bits: pool of 32-word blocks (or nullptr)
+  uint32_t* bit_next;                 // next block of a warp's chain
+  uint32_t* warp_first;               // first block of each light warp
+  uint32_t* pool_cursor;              // [kBitSubPools] allocation cursors
+  uint32_t pool_sub_blocks;           // blocks per sub-pool
   DevScalars* sc;
 };
 
@@ -82,7 +122,7 @@ cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const doubl
                                     const BandConst& bc, uint32_t* keys, uint32_t* idx,
                                     uint32_t* band_hist, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_band_layout(const BandConst& bc, const uint32_t* band_hist, BandLayout* lay,
-                               cudaStream_t st);
+                               HeavyMeta* meta, cudaStream_t st);
 // LSD radix sort of (key, val) pairs, 32-bit keys, stable.  Result lands in
 // (keys_a, vals_a).  tmp must hold radix_sort_tmp_bytes(n).
 size_t radix_sort_tmp_bytes(uint64_t n);
@@ -98,9 +138,19 @@ cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
 size_t scan_tmp_bytes(uint64_t n);
 cudaError_t exclusive_scan_u32_u64(uint32_t n, const uint32_t* in, uint64_t* out, void* tmp,
                                    unsigned long long* total_out, cudaStream_t st, int* launches);
+// Same with the element count read on the device (n_dev, clamped to n_cap).
+cudaError_t exclusive_scan_u32_u64_dev(uint64_t n_cap, const unsigned long long* n_dev,
+                                       const uint32_t* in, uint64_t* out, void* tmp,
+                                       unsigned long long* total_out, cudaStream_t st,
+                                       int* launches);
 
 enum QueryMode { QM_COUNT = 0, QM_EMIT = 1, QM_EMIT_BITS = 2 };
 cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const BandConst& bc,
                          cudaStream_t st);
+// Hub path: ranges -> slot scan -> chunking -> count (mode QM_COUNT) / emit.
+cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
+                              const BandConst& bc, void* scan_tmp, cudaStream_t st, int* launches);
+cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
+                         const BandConst& bc, cudaStream_t st);
 
 }  // namespace rhg
