@@ -24,6 +24,24 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Generate path: the points are re-derived from Philox(seed, i) (bit-identical to
+// K1, same device code) instead of gathering theta[i], r[i] at random addresses.
+__global__ void __launch_bounds__(256)
+    k_gather_philox(uint32_t n, uint64_t seed, double two_over_alpha, double half_span, double R,
+                    const uint32_t* __restrict__ sidx, PointRec* __restrict__ pts) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t i = sidx[k];
+    double th, rr;
+    words_to_point(vertex_words(seed, i), two_over_alpha, half_span, R, th, rr);
+    PointRec p;
+    p.theta = th;
+    p.s = sinh(rr);
+    p.a = exp(0.5 * rr);
+    p.b = exp(-0.5 * rr);
+    pts[k] = p;
+  }
+}
+
 // dir[dir_off[j] + b] = first sorted index of band j whose bucket >= b, for
 // b = 0 .. nb_j (entry nb_j = band end).  Thread k fills the entries in
 // (bucket(k-1), bucket(k)]; the last point of a band also fills the tail.
@@ -55,12 +73,16 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
-                               int L, PointRec* pts, uint32_t* dir, cudaStream_t st,
-                               int* launches) {
+                               int L, PointRec* pts, uint32_t* dir, const PhiloxPoints* gen,
+                               cudaStream_t st, int* launches) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  k_gather<<<blocks, 256, 0, st>>>(n, theta, r, sidx, pts);
+  if (gen)
+    k_gather_philox<<<blocks, 256, 0, st>>>(n, gen->seed, gen->two_over_alpha, gen->half_span,
+                                            gen->R, sidx, pts);
+  else
+    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, sidx, pts);
   k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
   if (launches) *launches += 2;
   return cudaGetLastError();

@@ -50,9 +50,6 @@ struct WarpSm {
   unsigned long long cur[32];
   uint32_t degc[32];
   uint32_t qid[32];
-  uint4 c_lo[32];                 // emit: certain ranges (lo0, lo1, lo2, n0) per lane
-  uint32_t c_n1[32];
-  uint32_t c_ex[32];              // emit: exclusive prefix of certain counts
 };
 
 struct BandSm {
@@ -175,7 +172,44 @@ struct SlabRanges {
   uint32_t clo[kCert], chi[kCert];  // certain edges
 };
 
-// Ranges of one query vertex (sorted position k, key q) in slab j.
+// Own slab: the undirected list keeps only partners sorted after v (DESIGN.md
+// Z9); CSR cuts v itself out of whichever range holds it.
+__device__ __forceinline__ void own_slab_cut(bool outward, uint32_t k, SlabRanges& rg) {
+    if (outward) {
+#pragma unroll
+      for (int x = 0; x < kTest; ++x) rg.tlo[x] = max(rg.tlo[x], min(k + 1, rg.thi[x]));
+#pragma unroll
+      for (int x = 0; x < kCert; ++x) rg.clo[x] = max(rg.clo[x], min(k + 1, rg.chi[x]));
+    } else {
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+        if (rg.clo[x] <= k && k < rg.chi[x]) {
+          rg.clo[2] = k + 1;
+          rg.chi[2] = rg.chi[x];
+          rg.chi[x] = k;
+        }
+      // test ranges: at most 3 of the 4 slots are in use (only one arc can wrap)
+#pragma unroll
+      for (int x = 0; x < kTest; ++x) {
+        if (rg.tlo[x] <= k && k < rg.thi[x]) {
+          const uint32_t tail_hi = rg.thi[x];
+          rg.thi[x] = k;
+          bool placed = false;
+#pragma unroll
+          for (int y = 0; y < kTest; ++y) {
+            if (!placed && y != x && !(rg.thi[y] > rg.tlo[y])) {
+              rg.tlo[y] = k + 1;
+              rg.thi[y] = tail_hi;
+              placed = true;
+            }
+          }
+        }
+      }
+    }
+}
+
+// Ranges of one query vertex (sorted position k, key q) in slab j (general
+// 64-bit version: hub vertices and slabs of >= 2^27 points).
 __device__ __forceinline__ void slab_ranges(int j, const BandConst& bc, const BandSm& B, uint32_t q,
                                             double qa, double qb, double qinv4s, uint32_t k,
                                             uint32_t qband, bool outward,
@@ -260,39 +294,115 @@ __device__ __forceinline__ void slab_ranges(int j, const BandConst& bc, const Ba
   } else {
     put_interval(ls, re, bstart, nj, rg.tlo, rg.thi, 0);
   }
-  if (j == (int)qband) {
-    if (outward) {  // undirected list: only partners sorted after v (Z9)
+  if (j == (int)qband) own_slab_cut(outward, k, rg);
+}
+
+
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// [a, b) in [0, 2 nj) relative positions -> <= 2 slab ranges (split at the seam nj)
+__device__ __forceinline__ void split_at_seam(int32_t a, int32_t b, int32_t nj, uint32_t bstart,
+                                              uint32_t& lo0, uint32_t& hi0, uint32_t& lo1,
+                                              uint32_t& hi1) {
+  if (b <= nj) {
+    lo0 = bstart + a; hi0 = bstart + b;
+  } else if (a >= nj) {
+    lo0 = bstart + (a - nj); hi0 = bstart + (b - nj);
+  } else {
+    lo0 = bstart + a; hi0 = bstart + nj;
+    lo1 = bstart; hi1 = bstart + (b - nj);
+  }
+}
+
+// Same ranges as slab_ranges (below), 32-bit positions (slabs < 2^27 points), MUFU
+// square roots (their ~2^-22 relative error is inside the 2^-12 / 2^-17 pads) and
+// the window numerators supplied by the caller: num = T4 - h(c_j)^2,
+// num1 = T4 - h(c_{j+1})^2 (num1 of slab j is num of slab j+1).
+__device__ __forceinline__ void slab_ranges_fast(int j, const BandConst& bc, const BandSm& B,
+                                                 int32_t q, double num, double num1,
+                                                 double qinv4s, uint32_t k, uint32_t qband,
+                                                 bool outward, const uint32_t* __restrict__ dir,
+                                                 SlabRanges& rg) {
+  const uint32_t bstart = B.start[j], bend = B.start[j + 1];
+  const int32_t nj = (int32_t)(bend - bstart);
 #pragma unroll
-      for (int x = 0; x < kTest; ++x) rg.tlo[x] = max(rg.tlo[x], min(k + 1, rg.thi[x]));
+  for (int x = 0; x < kTest; ++x) rg.tlo[x] = rg.thi[x] = bstart;
 #pragma unroll
-      for (int x = 0; x < kCert; ++x) rg.clo[x] = max(rg.clo[x], min(k + 1, rg.chi[x]));
-    } else {  // CSR: cut v itself out of whichever range holds it
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-        if (rg.clo[x] <= k && k < rg.chi[x]) {
-          rg.clo[2] = k + 1;
-          rg.chi[2] = rg.chi[x];
-          rg.chi[x] = k;
-        }
-      // test ranges: at most 3 of the 4 slots are in use (only one arc can wrap)
-#pragma unroll
-      for (int x = 0; x < kTest; ++x) {
-        if (rg.tlo[x] <= k && k < rg.thi[x]) {
-          const uint32_t tail_hi = rg.thi[x];
-          rg.thi[x] = k;
-          bool placed = false;
-#pragma unroll
-          for (int y = 0; y < kTest; ++y) {
-            if (!placed && y != x && !(rg.thi[y] > rg.tlo[y])) {
-              rg.tlo[y] = k + 1;
-              rg.thi[y] = tail_hi;
-              placed = true;
-            }
-          }
-        }
+  for (int x = 0; x < kCert; ++x) rg.clo[x] = rg.chi[x] = bstart;
+  // outer window at c_j: d_o >= 2 tan(dphi/2) K27 (1 + 2^-12) + 2
+  bool full = true;
+  int32_t d_o = 0;
+  const double invS = bc.invS[j];
+  if (invS != 0.0) {
+    const double ratio = __fma_rn(num, __dmul_rn(qinv4s, invS), __dmul_rn(qinv4s, bc.padS[j]));
+    if (ratio < 0.99) {
+      const float rf = fmaxf((float)ratio, 0.0f);
+      const float dqf = sqrt_approx(rf) * rsqrt_approx(1.0f - rf) *
+                        (2.0f * (float)RHG_Q27_SCALE * 1.000244140625f);
+      if (dqf < 67108860.0f) {
+        full = false;
+        d_o = (int32_t)dqf + 2;
       }
     }
   }
+  // certain window at c_{j+1}: d_i <= 2 sqrt(ratio1) K27 (1 - 2^-17) - 1
+  int32_t d_i = -1;
+  const double invS1 = bc.invS[j + 1];
+  if (invS1 != 0.0 && num >= bc.T4min && num1 >= bc.T4min) {
+    const float rf1 = fminf((float)__dmul_rn(num1, __dmul_rn(qinv4s, invS1)), 1.0f);
+    d_i = (int32_t)(sqrt_approx(rf1) * (2.0f * (float)RHG_Q27_SCALE * 0.99999237060546875f)) - 1;
+  }
+  const uint32_t sh = B.shift[j], off = B.dir_off[j];
+  const uint32_t lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
+  auto P = [&](int32_t bu) -> int32_t {  // unwrapped bucket -> unwrapped slab position
+    const int32_t per = bu >> lgnb;       // -1, 0 or 1
+    return (int32_t)(__ldg(dir + off + ((uint32_t)bu & nbm)) - bstart) + per * nj;
+  };
+  int32_t ls = 0, re = 0, cs = 0, ce = 0;
+  if (!full) {
+    ls = P((q - d_o) >> sh);
+    re = P(((q + d_o) >> sh) + 1);
+    if (re - ls >= nj) full = true;
+  }
+  bool cert = false;
+  if (d_i >= 0) {
+    cs = P(((q - d_i) >> sh) + 1);
+    ce = P((q + d_i) >> sh);
+    cert = ce > cs;
+  }
+  if (!cert) {
+    if (full) {
+      rg.thi[0] = bend;
+    } else {
+      const int32_t sft = ls < 0 ? nj : (ls >= nj ? -nj : 0);
+      split_at_seam(ls + sft, re + sft, nj, bstart, rg.tlo[0], rg.thi[0], rg.tlo[1], rg.thi[1]);
+    }
+  } else {
+    const int32_t sft = cs < 0 ? nj : (cs >= nj ? -nj : 0);
+    cs += sft; ce += sft;
+    split_at_seam(cs, ce, nj, bstart, rg.clo[0], rg.chi[0], rg.clo[1], rg.chi[1]);
+    if (full) {
+      split_at_seam(ce, cs + nj, nj, bstart, rg.tlo[0], rg.thi[0], rg.tlo[1], rg.thi[1]);
+    } else {
+      ls += sft; re += sft;
+      // [ls, cs) may dip below 0 and [ce, re) may pass 2 nj: shift them into range
+      if (ls < 0) split_at_seam(ls + nj, cs + nj, nj, bstart, rg.tlo[0], rg.thi[0], rg.tlo[1], rg.thi[1]);
+      else split_at_seam(ls, cs, nj, bstart, rg.tlo[0], rg.thi[0], rg.tlo[1], rg.thi[1]);
+      if (re > 2 * nj) split_at_seam(ce - nj, re - nj, nj, bstart, rg.tlo[2], rg.thi[2], rg.tlo[3], rg.thi[3]);
+      else split_at_seam(ce, re, nj, bstart, rg.tlo[2], rg.thi[2], rg.tlo[3], rg.thi[3]);
+    }
+  }
+  if (j == (int)qband) own_slab_cut(outward, k, rg);
 }
 
 __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long long o, uint32_t vid,
@@ -306,7 +416,7 @@ __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long lon
 //                  ballot words -> chained bit blocks
 //   QM_EMIT      : same sequence, re-tests (fallback when the bit pool ran dry)
 //   QM_EMIT_BITS : same sequence, replays the bits
-template <int MODE, int FMT>
+template <int MODE, int FMT, bool WIDE>
 __global__ void __launch_bounds__(QK_THREADS)
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   __shared__ WarpSm sm_all[QK_WARPS];
@@ -387,8 +497,13 @@ __global__ void __launch_bounds__(QK_THREADS)
     const uint32_t e = head + 1u + lane;
     uint32_t bit = 0;
     if (e < tail) {
-      const unsigned long long rel = sm.e_pref[e % RING] - consumed;
-      if (rel < 32ull) bit = 1u << (uint32_t)rel;
+      if (WIDE) {
+        const unsigned long long rel = sm.e_pref[e % RING] - consumed;
+        if (rel < 32ull) bit = 1u << (uint32_t)rel;
+      } else {  // ranges < 2^27: the 32 entries ahead start < 2^32 after `consumed`
+        const uint32_t rel = (uint32_t)sm.e_pref[e % RING] - (uint32_t)consumed;
+        if (rel < 32u) bit = 1u << rel;
+      }
     }
     const uint32_t M = __reduce_or_sync(FULL, bit);
     const uint32_t my_e = (head + __popc(M & ((2u << lane) - 1u))) % RING;
@@ -429,15 +544,33 @@ __global__ void __launch_bounds__(QK_THREADS)
     __syncwarp();
   };
 
+  // window numerator T4 - 4 sinh^2((r_v - c)/2) at c = c_j, carried from slab to slab
+  double num_j = 0.0;
+  if (!WIDE) {
+    const double h0 = __fma_rn(q.a, bc.B[jlo], -__dmul_rn(q.b, bc.A[jlo]));
+    num_j = __fma_rn(-h0, h0, T4);
+  }
   for (int j = jlo; j < bc.L; ++j) {
+    double num_j1 = 0.0;
+    if (!WIDE) {
+      const double h1 = __fma_rn(q.a, bc.B[j + 1], -__dmul_rn(q.b, bc.A[j + 1]));
+      num_j1 = __fma_rn(-h1, h1, T4);
+    }
+    const double num_here = num_j;
+    num_j = num_j1;
     if (bs.start[j] == bs.start[j + 1]) continue;
     SlabRanges rg;
 #pragma unroll
     for (int x = 0; x < kTest; ++x) rg.tlo[x] = rg.thi[x] = 0;
 #pragma unroll
     for (int x = 0; x < kCert; ++x) rg.clo[x] = rg.chi[x] = 0;
-    if (valid && (!outward || j >= (int)qband))
-      slab_ranges(j, bc, bs, qq, q.a, q.b, qinv4s, k, qband, outward, A.skey, A.dir, rg);
+    if (valid && (!outward || j >= (int)qband)) {
+      if (WIDE)
+        slab_ranges(j, bc, bs, qq, q.a, q.b, qinv4s, k, qband, outward, A.skey, A.dir, rg);
+      else
+        slab_ranges_fast(j, bc, bs, (int32_t)qq, num_here, num_j1, qinv4s, k, qband, outward,
+                         A.dir, rg);
+    }
     uint32_t cc[kCert];
     uint32_t ccs = 0;
 #pragma unroll
@@ -453,27 +586,32 @@ __global__ void __launch_bounds__(QK_THREADS)
       const uint32_t cinc = warp_incl(ccs);
       const uint32_t ctot = __shfl_sync(FULL, cinc, 31);
       if (ctot) {
+        const uint32_t cex = cinc - ccs;
         const unsigned long long cbase = sm.cur[lane];
-        sm.c_ex[lane] = cinc - ccs;
-        sm.c_lo[lane] = make_uint4(rg.clo[0], rg.clo[1], rg.clo[2], cc[0]);
-        sm.c_n1[lane] = cc[1];
-        __syncwarp();
+        const uint32_t cb_lo = (uint32_t)cbase, cb_hi = (uint32_t)(cbase >> 32);
         for (uint32_t t0 = 0; t0 < ctot; t0 += 32) {
           const uint32_t t = t0 + lane;
-          // owner lane: the last lane whose exclusive prefix is <= t
+          // owner lane: the last lane whose exclusive prefix is <= t (register search)
           uint32_t own = 0;
 #pragma unroll
-          for (uint32_t stp = 16; stp > 0; stp >>= 1)
-            if (sm.c_ex[own + stp] <= t) own += stp;
+          for (uint32_t stp = 16; stp > 0; stp >>= 1) {
+            const uint32_t p = __shfl_sync(FULL, cex, own + stp);
+            own = (p <= t) ? own + stp : own;
+          }
+          const uint32_t oex = __shfl_sync(FULL, cex, own);
+          const uint32_t n0 = __shfl_sync(FULL, cc[0], own), n1 = __shfl_sync(FULL, cc[1], own);
+          const uint32_t l0 = __shfl_sync(FULL, rg.clo[0], own);
+          const uint32_t l1 = __shfl_sync(FULL, rg.clo[1], own);
+          const uint32_t l2 = __shfl_sync(FULL, rg.clo[2], own);
+          const uint32_t blo = __shfl_sync(FULL, cb_lo, own), bhi = __shfl_sync(FULL, cb_hi, own);
+          const uint32_t ovid = __shfl_sync(FULL, qid, own);
           if (t < ctot) {
-            const uint4 d = sm.c_lo[own];
-            const uint32_t c1 = sm.c_n1[own];
-            const uint32_t r = t - sm.c_ex[own];
-            const uint32_t src = r < d.w ? d.x + r : (r < d.w + c1 ? d.y + (r - d.w) : d.z + (r - d.w - c1));
-            write_edge(A, sm.cur[own] + r, sm.qid[own], __ldg(A.sid + src), FMT);
+            const uint32_t r = t - oex;
+            const uint32_t src = r < n0 ? l0 + r : (r < n0 + n1 ? l1 + (r - n0) : l2 + (r - n0 - n1));
+            const unsigned long long ob = ((unsigned long long)bhi << 32) | blo;
+            write_edge(A, ob + r, ovid, __ldg(A.sid + src), FMT);
           }
         }
-        __syncwarp();
         sm.cur[lane] = cbase + ccs;
         __syncwarp();
       }
@@ -726,16 +864,23 @@ cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
   const uint32_t groups = (qa.n + 31) / 32;
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
+  const bool wide = qa.n >= (1u << 27);  // slabs may exceed 2^27 points: 64-bit positions
+#define RHG_LQ(M, F)                                                                   \
+  do {                                                                                 \
+    if (wide) k_query<M, F, true><<<blocks, QK_THREADS, 0, st>>>(qa, bc);              \
+    else k_query<M, F, false><<<blocks, QK_THREADS, 0, st>>>(qa, bc);                  \
+  } while (0)
   if (mode == QM_COUNT) {
-    if (fmt == RHG_CSR) k_query<QM_COUNT, RHG_CSR><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
-    else k_query<QM_COUNT, RHG_EDGES_UNDIRECTED><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
+    if (fmt == RHG_CSR) RHG_LQ(QM_COUNT, RHG_CSR);
+    else RHG_LQ(QM_COUNT, RHG_EDGES_UNDIRECTED);
   } else if (mode == QM_EMIT) {
-    if (fmt == RHG_CSR) k_query<QM_EMIT, RHG_CSR><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
-    else k_query<QM_EMIT, RHG_EDGES_UNDIRECTED><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
+    if (fmt == RHG_CSR) RHG_LQ(QM_EMIT, RHG_CSR);
+    else RHG_LQ(QM_EMIT, RHG_EDGES_UNDIRECTED);
   } else {
-    if (fmt == RHG_CSR) k_query<QM_EMIT_BITS, RHG_CSR><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
-    else k_query<QM_EMIT_BITS, RHG_EDGES_UNDIRECTED><<<blocks, QK_THREADS, 0, st>>>(qa, bc);
+    if (fmt == RHG_CSR) RHG_LQ(QM_EMIT_BITS, RHG_CSR);
+    else RHG_LQ(QM_EMIT_BITS, RHG_EDGES_UNDIRECTED);
   }
+#undef RHG_LQ
   return cudaGetLastError();
 }
 

@@ -8,37 +8,6 @@
 
 namespace rhg {
 
-// Philox4x32-10 (Salmon et al. 2011): counter (i_lo, i_hi, 0, 0), key = seed.
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-#pragma unroll
-  for (int round = 0; round < 10; ++round) {
-    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
-}
-
-__device__ __forceinline__ uint4 vertex_words(uint64_t seed, uint64_t i) {
-  return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
-                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-}
-
-// theta = fl(2pi) * u1, u1 = (w1:w0 >> 11) 2^-53  (Z10, Z12)
-// r = (2/alpha) asinh(sqrt(u2 * (cosh(alpha R) - 1)/2)), clamped to R (Z11)
-__device__ __forceinline__ void words_to_point(uint4 w, double two_over_alpha, double half_span,
-                                               double R, double& theta, double& r) {
-  uint64_t a = ((uint64_t)w.y << 32) | w.x;
-  uint64_t b = ((uint64_t)w.w << 32) | w.z;
-  double u1 = __dmul_rn((double)(a >> 11), 0x1.0p-53);
-  double u2 = __dmul_rn((double)(b >> 11), 0x1.0p-53);
-  theta = __dmul_rn(RHG_TWO_PI_HI, u1);
-  double rr = __dmul_rn(two_over_alpha, asinh(sqrt(__dmul_rn(u2, half_span))));
-  r = rr > R ? R : rr;
-}
-
 // Band j with c_j <= r < c_{j+1}; the last band is closed at R (Reading Z8).
 __device__ __forceinline__ uint32_t band_of(double r, const BandConst& bc) {
   int j = bc.L - 1;
@@ -204,12 +173,12 @@ cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint
   return cudaGetLastError();
 }
 
-cudaError_t launch_sample(uint64_t n, uint64_t seed, double alpha, double R, const BandConst& bc,
-                          double* theta, double* r, uint32_t* keys, uint32_t* idx,
-                          uint32_t* band_hist, cudaStream_t st) {
-  double half_span = (cosh(alpha * R) - 1.0) / 2.0;
-  k_sample<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, seed, 2.0 / alpha, half_span, bc, theta,
-                                                       r, keys, idx, band_hist);
+cudaError_t launch_sample(uint64_t n, const PhiloxPoints& gen, const BandConst& bc, double* theta,
+                          double* r, uint32_t* keys, uint32_t* idx, uint32_t* band_hist,
+                          cudaStream_t st) {
+  k_sample<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, gen.seed, gen.two_over_alpha,
+                                                       gen.half_span, bc, theta, r, keys, idx,
+                                                       band_hist);
   return cudaGetLastError();
 }
 

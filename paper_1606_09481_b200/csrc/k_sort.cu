@@ -32,53 +32,84 @@ __global__ void __launch_bounds__(RS_THREADS)
 
 // Stable scatter.  Warp w of block b owns items [b*TILE + w*512, +512) and walks
 // them in 16 rounds of 32; __match_any_sync ranks equal digits within a round.
+// The tile is then re-ordered by digit in shared memory and written out so that
+// consecutive threads store consecutive addresses of one digit run (coalesced).
 __global__ void __launch_bounds__(RS_THREADS)
     k_rs_scatter(uint32_t n, const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                  uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int shift,
                  const uint32_t* __restrict__ offs, uint32_t G) {
   __shared__ uint32_t wcnt[RS_WARPS][RS_RADIX];
+  __shared__ uint32_t tstart[RS_RADIX];
+  __shared__ uint32_t gbase[RS_RADIX];
+  __shared__ uint32_t wsum[RS_WARPS];
+  __shared__ uint32_t skey[RS_TILE];
+  __shared__ uint32_t sval[RS_TILE];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int d = lane; d < RS_RADIX; d += 32) wcnt[w][d] = 0;
   __syncwarp();
-  const uint32_t wbase = blockIdx.x * RS_TILE + w * (32 * RS_ITEMS);
+  const uint32_t tbase = blockIdx.x * RS_TILE;
+  const uint32_t wbase = tbase + w * (32 * RS_ITEMS);
   uint32_t key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
-    uint32_t i = wbase + it * 32 + lane;
-    bool valid = i < n;
+    const uint32_t i = wbase + it * 32 + lane;
+    const bool valid = i < n;
     key[it] = valid ? kin[i] : 0u;
     val[it] = valid ? vin[i] : 0u;
-    uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    uint32_t before = wcnt[w][d & 0xFFu];
+    const uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = wcnt[w][d & 0xFFu];
     loc[it] = before + __popc(peers & lt);
     __syncwarp();
     if (valid && (__ffs(peers) - 1) == lane) wcnt[w][d] = before + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps (warp order = item order => stable)
+  // per digit: exclusive prefix over warps (warp order = item order => stable),
+  // then the digit's start inside the tile (block scan over the 256 digit totals)
   {
-    int d = threadIdx.x;  // RS_THREADS == RS_RADIX
-    uint32_t run = offs[d * G + blockIdx.x];
+    const int d = threadIdx.x;  // RS_THREADS == RS_RADIX
+    uint32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
-      uint32_t c = wcnt[ww][d];
+      const uint32_t c = wcnt[ww][d];
       wcnt[ww][d] = run;
       run += c;
     }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) wpre += (ww < w) ? wsum[ww] : 0u;
+    tstart[d] = wpre + inc - run;
+    gbase[d] = offs[d * G + blockIdx.x];
   }
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
-    uint32_t i = wbase + it * 32 + lane;
+    const uint32_t i = wbase + it * 32 + lane;
     if (i < n) {
-      uint32_t d = (key[it] >> shift) & 0xFFu;
-      uint32_t pos = wcnt[w][d] + loc[it];
-      kout[pos] = key[it];
-      vout[pos] = val[it];
+      const uint32_t d = (key[it] >> shift) & 0xFFu;
+      const uint32_t lp = tstart[d] + wcnt[w][d] + loc[it];
+      skey[lp] = key[it];
+      sval[lp] = val[it];
     }
+  }
+  __syncthreads();
+  const uint32_t tn = (n - tbase) < (uint32_t)RS_TILE ? (n - tbase) : (uint32_t)RS_TILE;
+  for (uint32_t i = threadIdx.x; i < tn; i += RS_THREADS) {
+    const uint32_t k = skey[i];
+    const uint32_t d = (k >> shift) & 0xFFu;
+    const uint32_t gp = gbase[d] + (i - tstart[d]);
+    kout[gp] = k;
+    vout[gp] = sval[i];
   }
 }
 

@@ -55,10 +55,13 @@ rhg_status target_radius(double n, double kbar, double alpha, double* R) {
   return RHG_OK;
 }
 
+// "log n" slabs (base unstated; Z7): ceil(ln n).  The
+// edge set does not depend on L; ln n measured faster than log2 n on B200 (fewer
+// window evaluations per vertex, slightly more tests).
 int default_bands(uint64_t n) {
-  int L = 0;
-  while (L < 32 && (1ull << L) < n) ++L;  // ceil(log2 n)
-  return L < 1 ? 1 : L;
+  int L = (int)std::ceil(std::log((double)n));
+  if (L < 1) L = 1;
+  return L > kMaxBands ? kMaxBands : L;
 }
 
 // Slab boundaries: c_0 = 0, c_1 = (1-p)R/(1-p^L),
@@ -93,7 +96,9 @@ rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandCon
     bc->A[j] = std::exp(0.5 * bc->c[j]);
     bc->B[j] = std::exp(-0.5 * bc->c[j]);
     bc->invS[j] = bc->c[j] > 0.0 ? 1.0 / std::sinh(bc->c[j]) : 0.0;
+    bc->padS[j] = bc->T4 * 0x1.0p-48 * bc->invS[j];
   }
+  bc->T4min = bc->T4 * 0x1.0p-10;
   bc->heavy_threshold = (opt && opt->heavy_threshold) ? (double)opt->heavy_threshold : 1024.0;
   bc->heavy_cap = (uint32_t)heavy_cap_for(n);
   return RHG_OK;
@@ -273,10 +278,21 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   uint64_t* row_ptr_dev = host ? (uint64_t*)(ws + Lw.st_rowptr) : out->row_ptr;
   uint32_t* col_dev = host ? (uint32_t*)(ws + Lw.st_edges) : out->col;
   uint32_t* pairs_dev = host ? (uint32_t*)(ws + Lw.st_edges) : out->pairs;
-  // device-mode callers may keep the sampled points directly
-  if (sample && !host) {
-    if (out->theta_out) theta = out->theta_out;
-    if (out->r_out) r = out->r_out;
+  // Generate path: K1 stores the points only if the caller asked for them (the
+  // index build re-derives them from Philox); device-mode callers get them directly.
+  PhiloxPoints gen{};
+  if (sample) {
+    gen.seed = seed;
+    gen.two_over_alpha = 2.0 / alpha;
+    gen.half_span = (std::cosh(alpha * R) - 1.0) / 2.0;
+    gen.R = R;
+    if (host) {
+      if (!out->theta_out) theta = nullptr;
+      if (!out->r_out) r = nullptr;
+    } else {
+      theta = out->theta_out;
+      r = out->r_out;
+    }
   }
 
   Timer tm;
@@ -287,7 +303,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   CK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), st));
   float ms_h2d = 0;
   if (sample) {
-    CK(launch_sample(n, seed, alpha, R, bc, theta, r, keys_a, vals_a, hist, st));
+    CK(launch_sample(n, gen, bc, theta, r, keys_a, vals_a, hist, st));
     ++launches;
   } else {
     const double* th_src = theta_in;
@@ -311,8 +327,8 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   CK(radix_sort((uint32_t)n, keys_a, vals_a, keys_b, vals_b, ws + Lw.sort_tmp, 0, 32, st,
                 &launches));
   tm.mark();  // 2
-  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, dir, st,
-                        &launches));
+  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, dir,
+                        sample ? &gen : nullptr, st, &launches));
   tm.mark();  // 3
 
   QueryArgs qa{};
@@ -462,8 +478,8 @@ RHG_EXPORT rhg_status rhg_sample_points(uint64_t n, double alpha, double R, uint
   BandConst bc;
   rhg_status s = make_band_const(n < 2 ? 2 : n, R, nullptr, &bc);
   if (s != RHG_OK) return s;
-  CK(launch_sample(n, seed, alpha, R, bc, theta, r, nullptr, nullptr, nullptr,
-                   (cudaStream_t)stream));
+  PhiloxPoints gen{seed, 2.0 / alpha, (std::cosh(alpha * R) - 1.0) / 2.0, R};
+  CK(launch_sample(n, gen, bc, theta, r, nullptr, nullptr, nullptr, (cudaStream_t)stream));
   return RHG_OK;
 }
 

@@ -31,6 +31,8 @@ struct BandConst {
   double A[kMaxBands + 1];   // e^{c_j/2}, j = 0..L
   double B[kMaxBands + 1];   // e^{-c_j/2}
   double invS[kMaxBands + 1];// 1/sinh(c_j)   (0 for c_j = 0 -> full circle)
+  double padS[kMaxBands + 1];// T4 2^-48 / sinh(c_j): absolute upward pad of the window ratio
+  double T4min;              // 2^-10 T4: certain windows need T4 - h^2 above this at both ends
   double heavy_threshold;    // expected candidates per vertex above which a slab's vertices are hubs
   uint32_t heavy_cap;        // at most this many hub vertices (workspace bound)
 };
@@ -112,12 +114,52 @@ struct QueryArgs {
   DevScalars* sc;
 };
 
+// ---- K1 device code shared by the sampler and the generate-path gather ----
+// Philox4x32-10 (Salmon et al. 2011): counter (i_lo, i_hi, 0, 0), key = seed.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 vertex_words(uint64_t seed, uint64_t i) {
+  return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), 0u, 0u),
+                       make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+// theta = fl(2pi) * u1, u1 = (w1:w0 >> 11) 2^-53  (Z10, Z12)
+// r = (2/alpha) asinh(sqrt(u2 * (cosh(alpha R) - 1)/2)), clamped to R (Z11)
+__device__ __forceinline__ void words_to_point(uint4 w, double two_over_alpha, double half_span,
+                                               double R, double& theta, double& r) {
+  uint64_t a = ((uint64_t)w.y << 32) | w.x;
+  uint64_t b = ((uint64_t)w.w << 32) | w.z;
+  double u1 = __dmul_rn((double)(a >> 11), 0x1.0p-53);
+  double u2 = __dmul_rn((double)(b >> 11), 0x1.0p-53);
+  theta = __dmul_rn(RHG_TWO_PI_HI, u1);
+  double rr = __dmul_rn(two_over_alpha, asinh(sqrt(__dmul_rn(u2, half_span))));
+  r = rr > R ? R : rr;
+}
+
+
+// Parameters to re-derive the Philox points (generate path).
+struct PhiloxPoints {
+  uint64_t seed;
+  double two_over_alpha, half_span, R;
+};
+
 // ---- launch wrappers (each returns cudaError_t of the launch) ----
 cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out,
                                 cudaStream_t st);
-cudaError_t launch_sample(uint64_t n, uint64_t seed, double alpha, double R, const BandConst& bc,
-                          double* theta, double* r, uint32_t* keys, uint32_t* idx,
-                          uint32_t* band_hist, cudaStream_t st);
+// theta / r may be nullptr (not stored); keys == nullptr: sample the points only.
+cudaError_t launch_sample(uint64_t n, const PhiloxPoints& gen, const BandConst& bc, double* theta,
+                          double* r, uint32_t* keys, uint32_t* idx, uint32_t* band_hist,
+                          cudaStream_t st);
 cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const double* r,
                                     const BandConst& bc, uint32_t* keys, uint32_t* idx,
                                     uint32_t* band_hist, DevScalars* sc, cudaStream_t st);
@@ -129,10 +171,11 @@ size_t radix_sort_tmp_bytes(uint64_t n);
 cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
                        uint32_t* vals_b, void* tmp, int begin_bit, int end_bit, cudaStream_t st,
                        int* launches);
+// gen != nullptr: re-derive the points from Philox instead of reading theta / r.
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
-                               int L, PointRec* pts, uint32_t* dir, cudaStream_t st,
-                               int* launches);
+                               int L, PointRec* pts, uint32_t* dir, const PhiloxPoints* gen,
+                               cudaStream_t st, int* launches);
 // Exclusive scan of n uint32 counts into n+1 uint64 offsets (out[n] = total);
 // also writes the total into *total_out.  tmp: scan_tmp_bytes(n).
 size_t scan_tmp_bytes(uint64_t n);
