@@ -33,7 +33,8 @@ typedef struct CUstream_st *rhg_stream;
 
 typedef enum {
   RHG_OK = 0,
-  RHG_ERR_INVALID = 2,     /* bad argument: n < 2 or n >= 2^32, kbar <= 0, gamma <= 2 (alpha <= 1/2,
+  RHG_ERR_INVALID = 2,     /* bad argument: n < 2 or n >= 2^31 (the doubled point SoA is indexed
+                              with 32 bits; 2^31 points need > 180 GB anyway), kbar <= 0, gamma <= 2 (alpha <= 1/2,
                               PAPER.md:78), non-finite input, NULL required pointer */
   RHG_ERR_CALIBRATION = 3, /* getTargetRadius could not bracket kbar on the decreasing branch of
                               Eq. 22 */

@@ -9,18 +9,34 @@ namespace rhg {
 // Point record for sorted position k: theta, sinh r, e^{r/2}, e^{-r/2}.
 // (cosh d - 1 = 2 sinh^2((r_p - r_q)/2) + 2 sinh r_p sinh r_q sin^2(dphi/2), and
 //  2 sinh((r_p - r_q)/2) = e^{r_p/2} e^{-r_q/2} - e^{-r_p/2} e^{r_q/2}.)
+// Doubled SoA: the record of sorted position k in slab j (start s_j, n_j points)
+// is written at k + s_j and k + s_j + n_j, so slab j occupies [2 s_j, 2 s_j + 2 n_j)
+// as two back-to-back copies and every arc across 2 pi is one index range.
+__device__ __forceinline__ void put_doubled(uint32_t k, uint32_t key, const BandLayout* lay,
+                                            const PointRec& p, uint32_t id,
+                                            PointRec* __restrict__ pts, uint32_t* __restrict__ sid2) {
+  const uint32_t j = key >> kBandShift;
+  const uint32_t s = lay->start[j], nj = lay->start[j + 1] - s;
+  pts[k + s] = p;
+  pts[k + s + nj] = p;
+  sid2[k + s] = id;
+  sid2[k + s + nj] = id;
+}
+
 __global__ void __launch_bounds__(256)
     k_gather(uint32_t n, const double* __restrict__ theta, const double* __restrict__ r,
-             const uint32_t* __restrict__ sidx, PointRec* __restrict__ pts) {
+             const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
+             const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
+             uint32_t* __restrict__ sid2) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    uint32_t i = sidx[k];
-    double rr = r[i];
+    const uint32_t i = sidx[k];
+    const double rr = r[i];
     PointRec p;
     p.theta = theta[i];
     p.s = sinh(rr);
     p.a = exp(0.5 * rr);
     p.b = exp(-0.5 * rr);
-    pts[k] = p;
+    put_doubled(k, skey[k], lay, p, i, pts, sid2);
   }
 }
 
@@ -28,7 +44,9 @@ __global__ void __launch_bounds__(256)
 // K1, same device code) instead of gathering theta[i], r[i] at random addresses.
 __global__ void __launch_bounds__(256)
     k_gather_philox(uint32_t n, uint64_t seed, double two_over_alpha, double half_span, double R,
-                    const uint32_t* __restrict__ sidx, PointRec* __restrict__ pts) {
+                    const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
+                    const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
+                    uint32_t* __restrict__ sid2) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t i = sidx[k];
     double th, rr;
@@ -38,7 +56,7 @@ __global__ void __launch_bounds__(256)
     p.s = sinh(rr);
     p.a = exp(0.5 * rr);
     p.b = exp(-0.5 * rr);
-    pts[k] = p;
+    put_doubled(k, skey[k], lay, p, i, pts, sid2);
   }
 }
 
@@ -71,19 +89,70 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- query order (sector-major) ----
+// The light queries are processed sector by sector: all slabs' vertices with
+// angle in sector s (kQuerySectors equal arcs), slab by slab, before sector s+1.
+// The warps in flight then all read the candidates of one arc of every slab, so
+// each slab's points come from HBM about once per pass (slab-major order re-reads
+// every slab once per query slab, SURVEY E-9).  Cell c = s * L + j holds the
+// sorted positions of slab j in sector s (hub positions < heavy_end excluded).
+__global__ void k_query_cells(const uint32_t* __restrict__ skey, const BandLayout* __restrict__ lay,
+                              int L, uint32_t* __restrict__ cell_lo, uint32_t* __restrict__ cell_cnt) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (uint32_t)(kQuerySectors * L)) return;
+  const uint32_t sct = c / (uint32_t)L, j = c % (uint32_t)L;
+  const uint32_t b0 = lay->start[j], b1 = lay->start[j + 1];
+  auto lower = [&](uint32_t q) {  // first position of slab j with q27 >= q
+    uint32_t a = b0, b = b1;
+    while (a < b) {
+      const uint32_t m = (a + b) >> 1;
+      if ((skey[m] & kQMask) < q) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  const uint32_t sh = kQBits - kQuerySectorBits;
+  uint32_t lo = lower(sct << sh);
+  const uint32_t hi = (sct + 1 == (uint32_t)kQuerySectors) ? b1 : lower((sct + 1) << sh);
+  const uint32_t he = lay->heavy_end;
+  if (lo < he) lo = he;
+  cell_lo[c] = lo;
+  cell_cnt[c] = hi > lo ? hi - lo : 0u;
+}
+
+__global__ void __launch_bounds__(256)
+    k_query_fill(const uint32_t* __restrict__ cell_lo, const uint32_t* __restrict__ cell_cnt,
+                 const uint64_t* __restrict__ cell_off, uint32_t* __restrict__ order) {
+  const uint32_t c = blockIdx.x;
+  const uint32_t lo = cell_lo[c], cnt = cell_cnt[c];
+  const uint64_t o = cell_off[c];
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) order[o + t] = lo + t;
+}
+
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
-                               int L, PointRec* pts, uint32_t* dir, const PhiloxPoints* gen,
-                               cudaStream_t st, int* launches) {
+                               int L, PointRec* pts, uint32_t* sid2, uint32_t* dir,
+                               const PhiloxPoints* gen, cudaStream_t st, int* launches) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
   if (gen)
     k_gather_philox<<<blocks, 256, 0, st>>>(n, gen->seed, gen->two_over_alpha, gen->half_span,
-                                            gen->R, sidx, pts);
+                                            gen->R, skey, sidx, lay, pts, sid2);
   else
-    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, sidx, pts);
+    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, skey, sidx, lay, pts, sid2);
   k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query_order(const uint32_t* skey, const BandLayout* lay, int L,
+                               uint32_t* cell_lo, uint32_t* cell_cnt, uint64_t* cell_off,
+                               uint32_t* order, void* scan_tmp, cudaStream_t st, int* launches) {
+  const uint32_t cells = (uint32_t)(kQuerySectors * L);
+  k_query_cells<<<(cells + 255) / 256, 256, 0, st>>>(skey, lay, L, cell_lo, cell_cnt);
+  cudaError_t e = exclusive_scan_u32_u64(cells, cell_cnt, cell_off, scan_tmp, nullptr, st, launches);
+  if (e != cudaSuccess) return e;
+  k_query_fill<<<cells, 256, 0, st>>>(cell_lo, cell_cnt, cell_off, order);
   if (launches) *launches += 2;
   return cudaGetLastError();
 }

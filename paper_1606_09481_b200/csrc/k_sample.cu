@@ -157,7 +157,7 @@ __global__ void k_band_layout(const __grid_constant__ BandConst bc,
   if (j == 0) {
     uint32_t he = startJ < bc.heavy_cap ? startJ : bc.heavy_cap;
     lay->heavy_end = he;
-    meta->nslots = (unsigned long long)he * kRangesPerSlab * (unsigned long long)L;
+    meta->nvtx = he;
   }
 }
 

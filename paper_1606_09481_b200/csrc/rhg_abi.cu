@@ -108,16 +108,16 @@ rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandCon
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, dir, deg, offs,
+  size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, sid2, dir, deg, offs,
       scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
-  size_t h_start, h_len, h_lenw, h_soff, h_soffw, h_cc, h_choff, h_cslot, h_chits, h_cpos, h_meta,
-      h_bits;
-  size_t b_pool, b_next, b_first, b_cursor;
-  uint64_t nslots_cap, chunk_cap, hbits_cap, pool_blocks, pool_sub_blocks, light_warps;
+  size_t h_pstart, h_plen, h_poff, h_pword, h_np, h_vtot, h_vwords, h_vtot_off, h_vwbase, h_cc,
+      h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
+  size_t b_pool, b_next, b_first, b_cursor, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
+  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, pool_blocks, pool_sub_blocks, light_warps;
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
-constexpr uint64_t kChunkMin = 2048;
+constexpr uint64_t kChunkMin = 1024;
 
 int bands_for(uint64_t n, const rhg_options* opt) {
   return (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
@@ -127,8 +127,9 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   Layout L{};
   if (nbands < 1) nbands = 1;
   if (nbands > kMaxBands) nbands = kMaxBands;
-  L.nslots_cap = heavy_cap_for(n) * (uint64_t)kRangesPerSlab * (uint64_t)nbands;
-  L.chunk_cap = L.nslots_cap + kChunkExtra;
+  L.vcap = heavy_cap_for(n);
+  L.nslots_cap = L.vcap * (uint64_t)kRangesPerSlab * (uint64_t)nbands;
+  L.chunk_cap = L.vcap + kChunkExtra;
   // Candidate bits (emit replays them instead of re-testing).  Expected tests:
   // ~1.14 per directed CSR entry, ~1.2 per undirected edge (outward scan); sized
   // with margin from the output capacity.  Overflow falls back to re-testing.
@@ -136,7 +137,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.light_warps = (n + 31) / 32;
   L.pool_sub_blocks = (cap_tests / 1024 + L.light_warps + 64 * 16) / kBitSubPools + 1;
   L.pool_blocks = L.pool_sub_blocks * kBitSubPools;
-  L.hbits_cap = cap_tests / 64 + L.nslots_cap + 1024;
+  L.hbits_cap = cap_tests / 64 + L.nslots_cap / 2 + 1024;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -152,31 +153,42 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.sort_tmp = take(radix_sort_tmp_bytes(n));
   L.hist = take(4 * kMaxBands);
   L.lay = take(sizeof(BandLayout));
-  L.pts = take(sizeof(PointRec) * n);
+  L.pts = take(2 * sizeof(PointRec) * n);  // doubled SoA
+  L.sid2 = take(2 * 4 * n);
   L.dir = take(4 * (8 * n + 4 * kMaxBands + 8));  // <= 8 n_j + 1 entries per band
   L.deg = take(4 * n);
   L.offs = take(8 * (n + 1));
   {
     uint64_t m = n;
-    if (L.nslots_cap > m) m = L.nslots_cap;
+    if (L.vcap > m) m = L.vcap;
+    if ((uint64_t)kQuerySectors * kMaxBands > m) m = (uint64_t)kQuerySectors * kMaxBands;
     if (L.chunk_cap > m) m = L.chunk_cap;
     L.scan_tmp = take(scan_tmp_bytes(m));
   }
-  L.h_start = take(4 * L.nslots_cap);
-  L.h_len = take(4 * L.nslots_cap);
-  L.h_lenw = take(4 * L.nslots_cap);
-  L.h_soff = take(8 * (L.nslots_cap + 1));
-  L.h_soffw = take(8 * (L.nslots_cap + 1));
+  L.h_pstart = take(4 * L.nslots_cap);
+  L.h_plen = take(4 * L.nslots_cap);
+  L.h_poff = take(4 * L.nslots_cap);
+  L.h_pword = take(4 * L.nslots_cap);
+  L.h_np = take(4 * L.vcap);
+  L.h_vtot = take(4 * L.vcap);
+  L.h_vwords = take(4 * L.vcap);
+  L.h_vtot_off = take(8 * (L.vcap + 1));
+  L.h_vwbase = take(8 * (L.vcap + 1));
+  L.h_cc = take(4 * L.vcap);
+  L.h_choff = take(8 * (L.vcap + 1));
+  L.h_cvtx = take(4 * L.chunk_cap);
+  L.h_cpiece = take(4 * L.chunk_cap);
+  L.h_chits = take(4 * L.chunk_cap);
+  L.h_cpos = take(8 * (L.chunk_cap + 1));
   L.h_bits = take(4 * L.hbits_cap);
   L.b_pool = take(128 * L.pool_blocks);
   L.b_next = take(4 * L.pool_blocks);
   L.b_first = take(4 * L.light_warps);
   L.b_cursor = take(4 * kBitSubPools);
-  L.h_cc = take(4 * L.nslots_cap);
-  L.h_choff = take(8 * (L.nslots_cap + 1));
-  L.h_cslot = take(4 * L.chunk_cap);
-  L.h_chits = take(4 * L.chunk_cap);
-  L.h_cpos = take(8 * (L.chunk_cap + 1));
+  L.q_order = take(4 * n);
+  L.q_cell_lo = take(4 * kQuerySectors * kMaxBands);
+  L.q_cell_cnt = take(4 * kQuerySectors * kMaxBands);
+  L.q_cell_off = take(8 * (kQuerySectors * kMaxBands + 1));
   L.h_meta = take(sizeof(HeavyMeta));
   L.sc = take(sizeof(DevScalars));
   L.st_rowptr = host && f == RHG_CSR ? take(8 * (n + 1)) : o;
@@ -243,7 +255,7 @@ struct Timer {
 rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const double* theta_in,
                const double* r_in, double R, const rhg_output* out, cudaStream_t st) {
   if (!out || !out->num_edges) return RHG_ERR_INVALID;
-  if (n < 2 || n >= (1ull << 32)) return RHG_ERR_INVALID;
+  if (n < 2 || n >= (1ull << 31)) return RHG_ERR_INVALID;  // doubled positions < 2^32
   if (!(R >= 0.0) || !std::isfinite(R)) return RHG_ERR_INVALID;
   if (sample && (!(alpha > 0.5) || !std::isfinite(std::cosh(alpha * R)))) return RHG_ERR_INVALID;
   if (!std::isfinite(std::sinh(R / 2.0) * std::sinh(R / 2.0) * 4.0)) return RHG_ERR_INVALID;
@@ -271,6 +283,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   uint32_t* hist = (uint32_t*)(ws + Lw.hist);
   BandLayout* lay = (BandLayout*)(ws + Lw.lay);
   PointRec* pts = (PointRec*)(ws + Lw.pts);
+  uint32_t* sid2 = (uint32_t*)(ws + Lw.sid2);
   uint32_t* dir = (uint32_t*)(ws + Lw.dir);
   uint32_t* deg = (uint32_t*)(ws + Lw.deg);
   uint64_t* offs_ws = (uint64_t*)(ws + Lw.offs);
@@ -327,8 +340,11 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   CK(radix_sort((uint32_t)n, keys_a, vals_a, keys_b, vals_b, ws + Lw.sort_tmp, 0, 32, st,
                 &launches));
   tm.mark();  // 2
-  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, dir,
+  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, sid2, dir,
                         sample ? &gen : nullptr, st, &launches));
+  CK(launch_query_order(keys_a, lay, bc.L, (uint32_t*)(ws + Lw.q_cell_lo),
+                        (uint32_t*)(ws + Lw.q_cell_cnt), (uint64_t*)(ws + Lw.q_cell_off),
+                        (uint32_t*)(ws + Lw.q_order), ws + Lw.scan_tmp, st, &launches));
   tm.mark();  // 3
 
   QueryArgs qa{};
@@ -336,9 +352,10 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.pts = pts;
   qa.skey = keys_a;
   qa.sid = vals_a;
+  qa.sid2 = sid2;
   qa.dir = dir;
   qa.lay = lay;
-  qa.order = nullptr;
+  qa.order = (const uint32_t*)(ws + Lw.q_order);
   qa.bits = (uint32_t*)(ws + Lw.b_pool);
   qa.bit_next = (uint32_t*)(ws + Lw.b_next);
   qa.warp_first = (uint32_t*)(ws + Lw.b_first);
@@ -349,20 +366,25 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.deg = deg;
   qa.sc = sc;
   HeavyArgs ha{};
-  ha.start = (uint32_t*)(ws + Lw.h_start);
-  ha.len = (uint32_t*)(ws + Lw.h_len);
-  ha.lenw = (uint32_t*)(ws + Lw.h_lenw);
-  ha.soff = (uint64_t*)(ws + Lw.h_soff);
-  ha.soffw = (uint64_t*)(ws + Lw.h_soffw);
-  ha.bits = (uint32_t*)(ws + Lw.h_bits);
-  ha.bits_cap = Lw.hbits_cap;
+  ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
+  ha.plen = (uint32_t*)(ws + Lw.h_plen);
+  ha.poff = (uint32_t*)(ws + Lw.h_poff);
+  ha.pword = (uint32_t*)(ws + Lw.h_pword);
+  ha.np = (uint32_t*)(ws + Lw.h_np);
+  ha.vtot = (uint32_t*)(ws + Lw.h_vtot);
+  ha.vwords = (uint32_t*)(ws + Lw.h_vwords);
+  ha.vtot_off = (uint64_t*)(ws + Lw.h_vtot_off);
+  ha.vwbase = (uint64_t*)(ws + Lw.h_vwbase);
   ha.cc = (uint32_t*)(ws + Lw.h_cc);
   ha.choff = (uint64_t*)(ws + Lw.h_choff);
-  ha.chunk_slot = (uint32_t*)(ws + Lw.h_cslot);
+  ha.chunk_vtx = (uint32_t*)(ws + Lw.h_cvtx);
+  ha.chunk_piece = (uint32_t*)(ws + Lw.h_cpiece);
   ha.chunk_hits = (uint32_t*)(ws + Lw.h_chits);
   ha.chunk_pos = (uint64_t*)(ws + Lw.h_cpos);
+  ha.bits = (uint32_t*)(ws + Lw.h_bits);
+  ha.bits_cap = Lw.hbits_cap;
   ha.meta = hmeta;
-  ha.nslots_cap = (uint64_t)bc.heavy_cap * kRangesPerSlab * (uint64_t)bc.L;
+  ha.vcap = Lw.vcap;
   ha.chunk_cap = Lw.chunk_cap;
   ha.chunk_min = kChunkMin;
   CK(launch_heavy_plan(f, qa, ha, bc, ws + Lw.scan_tmp, st, &launches));

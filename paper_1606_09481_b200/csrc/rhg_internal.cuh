@@ -13,8 +13,11 @@ constexpr int kBandShift = 27;         // sort key = band << 27 | q27(theta)
 constexpr uint32_t kQBits = 27;
 constexpr uint32_t kQMax = (1u << kQBits) - 1u;
 constexpr uint32_t kQMask = kQMax;
-constexpr uint32_t kBitSubPools = 64;  // light-warp bit blocks come from 64 sub-pools
-constexpr uint32_t kRangesPerSlab = 7;  // per (vertex, slab): 4 pieces to test + 3 certain
+constexpr uint32_t kBitSubPools = 64;
+constexpr int kQuerySectorBits = 8;    // light queries run sector-major over 2^8 angular sectors
+constexpr int kQuerySectors = 1 << kQuerySectorBits;  // light-warp bit blocks come from 64 sub-pools
+constexpr uint32_t kRangesPerSlab = 6;  // hub slots per (vertex, slab): 4 pieces to test + 2 certain
+constexpr uint32_t kTestPieces = 4;
 
 // fl(2*pi) and the remainder 2*pi - fl(2*pi): seam differences (Z13)
 #define RHG_TWO_PI_HI 0x1.921fb54442d18p+2
@@ -48,33 +51,42 @@ struct BandLayout {
   float expected[kMaxBands];       // upper bound of E[candidates] for a vertex of band j
 };
 
-// Hub ("heavy") vertices: per (vertex, slab, wrap part) range slots, split into
-// fixed-size chunks that are spread over the whole GPU.
+// Hub ("heavy") vertices: their (slab, piece) candidate ranges are materialised
+// as compacted pieces per vertex, and each vertex's concatenated candidate
+// sequence is cut into fixed-size chunks that are spread over the whole GPU.
 struct HeavyMeta {
-  unsigned long long nslots;   // heavy_end * kRangesPerSlab * L
-  unsigned long long cand;     // total candidates in the slots
+  unsigned long long nvtx;     // hub vertices (= heavy_end)
+  unsigned long long cand;     // total candidates (tested + certain) of hub vertices
   unsigned long long nchunks;  // total chunks
-  unsigned long long chunk;    // chunk size (candidates)
-  unsigned long long hits;     // total hits (directed / outward edges) of hub vertices
-  unsigned long long words;    // candidate-bit words of the hub slots
+  unsigned long long chunk;    // chunk size (candidates, multiple of 32)
+  unsigned long long hits;     // total edges of hub vertices (directed / outward)
+  unsigned long long words;    // candidate-bit words of the tested pieces
   unsigned int bits_overflow;  // words > bits_cap: the hub emit re-tests
 };
 
+constexpr uint32_t kCertainPiece = 0x80000000u;  // plen flag: every candidate is an edge
+
 struct HeavyArgs {
-  uint32_t* start;          // [nslots_cap] first candidate (sorted position)
-  uint32_t* len;            // [nslots_cap] candidates in the slot
-  uint32_t* lenw;           // [nslots_cap] bit words of the slot (ceil(len/32))
-  uint64_t* soff;           // [nslots_cap + 1] scan of len
-  uint64_t* soffw;          // [nslots_cap + 1] scan of lenw
-  uint32_t* bits;           // [bits_cap] hub candidate bits
-  uint64_t bits_cap;
-  uint32_t* cc;             // [nslots_cap] chunks per slot
-  uint64_t* choff;          // [nslots_cap + 1] scan of cc
-  uint32_t* chunk_slot;     // [chunk_cap] slot of each chunk
+  // per hub vertex i, pieces [i * LS, i * LS + np[i]) (LS = kRangesPerSlab * L)
+  uint32_t* pstart;         // first doubled position of the piece
+  uint32_t* plen;           // candidates | kCertainPiece
+  uint32_t* poff;           // offset of the piece in the vertex's candidate sequence
+  uint32_t* pword;          // offset of the piece's bit words in the vertex's words
+  uint32_t* np;             // [vcap] pieces
+  uint32_t* vtot;           // [vcap] candidates
+  uint32_t* vwords;         // [vcap] bit words
+  uint64_t* vtot_off;       // [vcap + 1] scan of vtot (total -> meta->cand)
+  uint64_t* vwbase;         // [vcap + 1] scan of vwords
+  uint32_t* cc;             // [vcap] chunks per vertex
+  uint64_t* choff;          // [vcap + 1] scan of cc
+  uint32_t* chunk_vtx;      // [chunk_cap]
+  uint32_t* chunk_piece;    // [chunk_cap] first piece the chunk touches
   uint32_t* chunk_hits;     // [chunk_cap]
   uint64_t* chunk_pos;      // [chunk_cap + 1] scan of chunk_hits
+  uint32_t* bits;           // [bits_cap] hub candidate bits
+  uint64_t bits_cap;
   HeavyMeta* meta;
-  uint64_t nslots_cap;
+  uint64_t vcap;
   uint64_t chunk_cap;
   uint64_t chunk_min;       // minimum chunk size
 };
@@ -96,12 +108,13 @@ struct __align__(16) PointRec {
 
 struct QueryArgs {
   uint32_t n;
-  const PointRec* __restrict__ pts;   // sorted by (band, theta)
-  const uint32_t* __restrict__ skey;  // sorted keys
-  const uint32_t* __restrict__ sid;   // sorted position -> vertex id
+  const PointRec* __restrict__ pts;   // doubled SoA: slab j at [2 start_j, 2 start_j + 2 n_j), two copies
+  const uint32_t* __restrict__ skey;  // sorted keys [n]
+  const uint32_t* __restrict__ sid;   // sorted position -> vertex id [n]
+  const uint32_t* __restrict__ sid2;  // doubled position -> vertex id [2n]
   const uint32_t* __restrict__ dir;   // bucket directory
   const BandLayout* __restrict__ lay;
-  const uint32_t* __restrict__ order; // query order (sorted positions), or nullptr = identity
+  const uint32_t* __restrict__ order; // light query order: sorted positions, sector-major [n - heavy_end]
   uint32_t* deg;                      // count pass: degree per vertex id
   const uint64_t* __restrict__ offs;  // emit pass: output offset per vertex id
   uint32_t* col;                      // CSR output
@@ -172,10 +185,17 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
                        uint32_t* vals_b, void* tmp, int begin_bit, int end_bit, cudaStream_t st,
                        int* launches);
 // gen != nullptr: re-derive the points from Philox instead of reading theta / r.
+// pts / sid2: the doubled SoA (2n entries; slab j stored twice back to back at
+// [2 start_j, 2 start_j + 2 n_j), so any arc of the slab is one index range).
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
-                               int L, PointRec* pts, uint32_t* dir, const PhiloxPoints* gen,
-                               cudaStream_t st, int* launches);
+                               int L, PointRec* pts, uint32_t* sid2, uint32_t* dir,
+                               const PhiloxPoints* gen, cudaStream_t st, int* launches);
+// Sector-major order of the light queries (k_index.cu); cell arrays hold
+// kQuerySectors * L entries (cell_off: + 1).
+cudaError_t launch_query_order(const uint32_t* skey, const BandLayout* lay, int L,
+                               uint32_t* cell_lo, uint32_t* cell_cnt, uint64_t* cell_off,
+                               uint32_t* order, void* scan_tmp, cudaStream_t st, int* launches);
 // Exclusive scan of n uint32 counts into n+1 uint64 offsets (out[n] = total);
 // also writes the total into *total_out.  tmp: scan_tmp_bytes(n).
 size_t scan_tmp_bytes(uint64_t n);

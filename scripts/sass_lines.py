@@ -1,7 +1,7 @@
 """Join an ncu SASS-level source page (csv) with nvdisasm -g line info:
 per-source-line instruction executions and stall samples for one kernel."""
 import csv, re, sys, collections
-sass_file, ncu_csv, kernel_sym, kernel_pat = sys.argv[1:5]
+sass_file, ncu_csv, kernel_sym, kernel_pat = sys.argv[1:5]  # [top-N]
 lines = open(sass_file).read().split('\n')
 start = next(i for i, l in enumerate(lines) if l.startswith('.text.' + kernel_sym + ':'))
 cur = None; seq = []
@@ -25,5 +25,5 @@ for k in range(n):
     src = seq[k][0]
     agg[src] += int(b['rows'][k][ie] or 0); st[src] += int(b['rows'][k][ss] or 0)
 tot = sum(agg.values()); tst = sum(st.values())
-for src, v in sorted(agg.items(), key=lambda x: -x[1])[:40]:
+for src, v in sorted(agg.items(), key=lambda x: -x[1])[:int(sys.argv[5]) if len(sys.argv) > 5 else 40]:
     print(f'{src}  exec {100*v/tot:5.1f}%  stall {100*st[src]/tst:5.1f}%')
