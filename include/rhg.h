@@ -92,8 +92,8 @@ typedef struct {
         graph in `workspace` and copies it with cudaMemcpyAsync on `stream`. */
   int host_buffers;
   uint64_t *row_ptr;       /* CSR: n+1 entries (row_ptr[n] = number of directed edges)        */
-  uint32_t *col;           /* CSR: capacity_edges entries                                      */
-  uint32_t *pairs;         /* EDGES_UNDIRECTED: 2*capacity_edges entries                       */
+  uint32_t *col;           /* CSR: capacity_edges entries; device buffers 32-byte aligned       */
+  uint32_t *pairs;         /* EDGES_UNDIRECTED: 2*capacity_edges entries; device: 32-byte aligned */
   uint64_t capacity_edges; /* CSR: directed entries col can hold; pairs: undirected edges      */
   void *workspace;         /* device scratch, caller-owned, >= rhg_workspace_bytes(...)        */
   size_t workspace_bytes;

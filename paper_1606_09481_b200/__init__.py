@@ -18,7 +18,9 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librhg.so")
+# RHG_LIB_PATH: an alternative build of the same library (experiments, scripts/);
+# there is no other implementation behind it.
+LIB_PATH = os.environ.get("RHG_LIB_PATH", os.path.join(_HERE, "librhg.so"))
 
 RHG_OK, RHG_ERR_INVALID, RHG_ERR_CALIBRATION, RHG_ERR_WORKSPACE = 0, 2, 3, 4
 RHG_ERR_CAPACITY, RHG_ERR_DOMAIN, RHG_ERR_CUDA = 5, 6, 7

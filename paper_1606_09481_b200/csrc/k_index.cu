@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dir[dir_off[j] + b] = first sorted index of band j whose bucket >= b, for
+// dir[dir_off[j] + b] = first position of band j (relative to the band start)
+// whose bucket >= b, for
 // b = 0 .. nb_j (entry nb_j = band end).  Thread k fills the entries in
 // (bucket(k-1), bucket(k)]; the last point of a band also fills the tail.
 __global__ void __launch_bounds__(256)
@@ -73,10 +74,11 @@ __global__ void __launch_bounds__(256)
     uint32_t b = (key & kQMask) >> sh;
     int64_t prev = -1;
     if (k > lay->start[j]) prev = (int64_t)((skey[k - 1] & kQMask) >> sh);
-    for (int64_t bb = prev + 1; bb <= (int64_t)b; ++bb) dir[off + bb] = k;
+    const uint32_t rel = k - lay->start[j];
+    for (int64_t bb = prev + 1; bb <= (int64_t)b; ++bb) dir[off + bb] = rel;
     if (k + 1 == lay->start[j + 1]) {
       uint32_t nb = lay->nb[j];
-      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
+      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = rel + 1;
     }
   }
   // empty bands: both entries = band start
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(256)
     int j = threadIdx.x;
     if (lay->count[j] == 0) {
       uint32_t off = lay->dir_off[j], nb = lay->nb[j];
-      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = lay->start[j];
+      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = 0u;
     }
   }
 }

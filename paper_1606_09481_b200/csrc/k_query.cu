@@ -62,8 +62,8 @@ struct __align__(16) CRec {
 };
 
 struct WarpSm {
-  double2 qA[32];  // (theta, 4 sinh r)
-  double2 qB[32];  // (e^{r/2}, e^{-r/2})
+  double2 qA[2];   // per group vertex: (theta, 4 sinh r)
+  double2 qB[2];   // (e^{r/2}, e^{-r/2})
   QRec rec[32];
   XRec xr[32];
   CRec cr[32];
@@ -211,7 +211,7 @@ __device__ __forceinline__ void slab_window(int j, const BandConst& bc, const Ba
   const uint32_t lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
   auto P = [&](I bu) -> I {  // bu >> lgnb is -1, 0 or 1
     const I per = bu >> lgnb;
-    return (I)(__ldg(dir + off + ((uint32_t)bu & nbm)) - bstart) + (per < 0 ? -nj : (per > 0 ? nj : (I)0));
+    return (I)__ldg(dir + off + ((uint32_t)bu & nbm)) + (per < 0 ? -nj : (per > 0 ? nj : (I)0));
   };
   I ls = 0, re = 0, cs = 0, ce = 0;
   if (!full) {
@@ -252,6 +252,62 @@ __device__ __forceinline__ void slab_window(int j, const BandConst& bc, const Ba
   }
 }
 
+// Per-slab constants of the light kernel, staged in shared memory.
+struct SlabC {
+  double invS, padS;      // 1/sinh c_j (0 for c_j = 0), T4 2^-48 / sinh c_j
+  double A0, B0;          // e^{c_j/2}, e^{-c_j/2}
+  double A1, B1, invS1;   // e^{c_{j+1}/2}, e^{-c_{j+1}/2}, 1/sinh c_{j+1}
+  uint32_t start, nj, off, sh;
+};
+
+// slab_window for slabs of < 2^30 points, written for few instructions: the same
+// windows, pads and bucket rounding, with selects instead of branches.
+__device__ __forceinline__ void win32(const SlabC& S, int32_t q, double num, double num1,
+                                      double qinv4s, double T4min,
+                                      const uint32_t* __restrict__ dir, SlabWin<int32_t>& w) {
+  const int32_t nj = (int32_t)S.nj;
+  // outer window at c_j: d_o >= 2 tan(dphi/2) K27 (1 + 2^-12) + 2 quanta
+  const double ratio = __dmul_rn(qinv4s, __fma_rn(num, S.invS, S.padS));
+  bool full = !(ratio < 0.99) || S.invS == 0.0;
+  const float rf = fminf(fmaxf((float)ratio, 0.0f), 0.99f);
+  const float dqf = sqrt_approx(rf) * rsqrt_approx(1.0f - rf) *
+                    (2.0f * (float)RHG_Q27_SCALE * 1.000244140625f);
+  full = full || !(dqf < 67108860.0f);
+  const int32_t d_o = full ? 0 : (int32_t)dqf + 2;
+  // certain window at c_{j+1}: d_i <= 2 sqrt(ratio1) K27 (1 - 2^-17) - 1 quantum
+  const bool certok = S.invS1 != 0.0 && num >= T4min && num1 >= T4min;
+  const float rf1 = fminf((float)__dmul_rn(num1, __dmul_rn(qinv4s, S.invS1)), 1.0f);
+  const int32_t d_i =
+      certok ? (int32_t)(sqrt_approx(rf1) * (2.0f * (float)RHG_Q27_SCALE * 0.99999237060546875f)) - 1
+             : -1;
+  const uint32_t sh = S.sh, lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
+  const uint32_t* __restrict__ D = dir + S.off;
+  auto P = [&](int32_t bu) -> int32_t {  // unwrapped bucket -> unwrapped position
+    return (int32_t)__ldg(D + ((uint32_t)bu & nbm)) + (bu >> lgnb) * nj;
+  };
+  int32_t ls = P((q - d_o) >> sh), re = P(((q + d_o) >> sh) + 1);
+  full = full || (re - ls >= nj);
+  int32_t cs = P(((q - d_i) >> sh) + 1), ce = P((q + d_i) >> sh);  // d_i = -1: ce <= cs
+  const bool cert = ce > cs;
+  const int32_t base = full ? cs : ls;  // shift the arc so that it starts in the first copy
+  const int32_t sft = base < 0 ? nj : (base >= nj ? -nj : 0);
+  ls += sft; re += sft; cs += sft; ce += sft;
+  if (!cert) ce = cs;
+  // non-full: test [ls, re) minus [cs, ce); full: test [ce, cs + nj) (or all of it)
+  w.cs = cert ? cs : 0;
+  w.ce = cert ? ce : 0;
+  if (full) {
+    w.a = cert ? ce : 0;
+    w.b = cert ? cs + nj : nj;
+    w.h0 = w.h1 = w.b;
+  } else {
+    w.a = ls;
+    w.b = re;
+    w.h0 = cert ? cs : re;
+    w.h1 = cert ? ce : re;
+  }
+}
+
 // [x, y) minus the periodic exclusion [e1, e1 + wx) u [e1 + nj, e1 + nj + wx)
 // (y - x <= nj, so at most two pieces survive).  CSR: e1 = own position, wx = 1
 // (no self-loop); undirected list: e1 = 0, wx = own position + 1 (only partners
@@ -271,9 +327,30 @@ __device__ __forceinline__ void cut_piece(I x, I y, I e1, I wx, I nj, I& lo0, I&
   }
 }
 
+// L2 policy for the id array sid2: it is re-read by every neighbourhood, while the
+// output streams 4-8 GB through L2, so keep it resident (evict_last).
+__device__ __forceinline__ uint64_t policy_keep() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* ptr, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+constexpr int kCopyUnroll = 4;
+
 template <int FMT>
 __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long long o, uint32_t vid,
                                            uint32_t w) {
+#if defined(RHG_EXP) && RHG_EXP == 1  // experiment: no output stores (loads kept alive)
+  if (w == 0xFFFFFFFFu && o == 0) A.col[0] = w;
+  return;
+#elif defined(RHG_EXP) && RHG_EXP == 3  // experiment: every thread stores to its own slot
+  A.col[(blockIdx.x * blockDim.x + threadIdx.x) & 0xFFFFFu] = w;
+  return;
+#endif
   if (FMT == RHG_CSR) A.col[o] = w;
   else reinterpret_cast<uint2*>(A.pairs)[o] = vid < w ? make_uint2(vid, w) : make_uint2(w, vid);
 }
@@ -286,241 +363,274 @@ __device__ __forceinline__ uint32_t lane_range_mask(int lo, int hi) {
 }
 
 // Light vertices: one warp per 32 consecutive entries of the sector-major query
-// order (sorted positions >= heavy_end).
-//   QM_COUNT     : certain pieces counted, annulus candidates tested; deg[v];
-//                  ballot words -> chained bit blocks
-//   QM_EMIT      : same sequence, re-tests (fallback when the bit pool ran dry)
-//   QM_EMIT_BITS : same sequence, replays the bits
+// order, one vertex per lane, slabs in lock step.  Per slab every lane computes
+// its window (the paper's per-vertex loop body) and then walks
+// its own candidates sequentially: certain pieces are copied, the annulus is
+// tested exactly.  A lane writes only its own row, through an 8-word shared-memory
+// stage, so rows leave the SM as whole 32-byte sectors (one STG.256 each).
+//   QM_COUNT     : deg[v]; test results as bits, word w of lane l of warp g at
+//                  bits[(g * kLightBitRows + w) * 32 + l] (warp_over[g] = 1 if
+//                  some lane needs more than kLightBitRows words)
+//   QM_EMIT      : writes the rows, re-testing
+//   QM_EMIT_BITS : writes the rows, replaying the bits (re-tests warps with warp_over)
+constexpr int kStageStride = 17;  // 16-word ring per lane (+1: bank-conflict-free)
+
+template <int FMT>
+struct RowWriter {
+  // CSR: 8 ids per 32-byte sector; pairs: 4 (u, v) pairs per sector.  The stage is
+  // a two-sector ring; a sector goes out (one STG.256) when the next one starts.
+  static constexpr uint32_t EPS = FMT == RHG_CSR ? 8u : 4u;
+  uint32_t* stage;                 // this lane's ring (16 words)
+  unsigned long long pos, start;   // next slot, first slot of the row (elements)
+  __device__ __forceinline__ void store_elem(uint32_t slot, uint32_t vid, uint32_t w) {
+    if (FMT == RHG_CSR) {
+      stage[slot] = w;
+    } else {
+      stage[2 * slot] = vid < w ? vid : w;
+      stage[2 * slot + 1] = vid < w ? w : vid;
+    }
+  }
+  __device__ __forceinline__ void write_elems(const QueryArgs& A, unsigned long long s0,
+                                              const uint32_t* r, uint32_t lo, uint32_t hi) {
+    for (uint32_t x = lo; x < hi; ++x) {
+      if (FMT == RHG_CSR) A.col[s0 + x] = r[x];
+      else reinterpret_cast<uint2*>(A.pairs)[s0 + x] = make_uint2(r[2 * x], r[2 * x + 1]);
+    }
+  }
+  __device__ __forceinline__ void flush(const QueryArgs& A, unsigned long long sec) {
+    const uint32_t* r = stage + (uint32_t)(sec & 1) * 8u;
+    const unsigned long long s0 = sec * EPS;
+    if (s0 >= start) {
+      uint32_t* dst = FMT == RHG_CSR ? A.col + s0 : A.pairs + 2 * s0;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]),
+                   "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                   : "memory");
+    } else {  // first sector of the row: the slots before `start` belong to the previous row
+      write_elems(A, s0, r, (uint32_t)(start - s0), EPS);
+    }
+  }
+  // append w[lo..hi) (hi - lo <= 4)
+  __device__ __forceinline__ void put4(const QueryArgs& A, uint32_t vid, const uint32_t* w,
+                                       uint32_t lo, uint32_t hi) {
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u)
+      if (u >= lo && u < hi) store_elem((uint32_t)(pos + (u - lo)) & (2 * EPS - 1), vid, w[u]);
+    const unsigned long long old = pos;
+    pos += hi - lo;
+    if ((old / EPS) != (pos / EPS)) flush(A, old / EPS);  // a sector completed
+  }
+  __device__ __forceinline__ void put(const QueryArgs& A, uint32_t vid, uint32_t w) {
+    store_elem((uint32_t)pos & (2 * EPS - 1), vid, w);
+    ++pos;
+    if ((pos & (EPS - 1)) == 0) flush(A, pos / EPS - 1);
+  }
+  __device__ __forceinline__ void finish(const QueryArgs& A) {
+    const uint32_t x = (uint32_t)pos & (EPS - 1);
+    if (x) {
+      const unsigned long long sec = pos / EPS, s0 = sec * EPS;
+      write_elems(A, s0, stage + (uint32_t)(sec & 1) * 8u, s0 >= start ? 0u : (uint32_t)(start - s0), x);
+    }
+  }
+};
+
+__device__ __forceinline__ uint4 ld4_keep(const uint32_t* ptr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+
+// 1 / (4 sinh r) to ~1 ulp: float reciprocal + two Newton steps (the window pads
+// absorb far larger relative errors)
+__device__ __forceinline__ double inv4s_of(double s) {
+  const double y = 4.0 * s;
+  double x = (double)__frcp_rn((float)y);
+  x = __fma_rn(x, __fma_rn(-y, x, 1.0), x);
+  x = __fma_rn(x, __fma_rn(-y, x, 1.0), x);
+  return x;
+}
+
 template <int MODE, int FMT, bool WIDE>
 __global__ void __launch_bounds__(QK_THREADS)
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
-  __shared__ WarpSm sm_all[QK_WARPS];
   __shared__ BandSm bs;
+  __shared__ SlabC scs[kMaxBands];
+  __shared__ uint32_t stage_all[MODE == QM_COUNT ? 1 : QK_THREADS * kStageStride];
   load_band_sm(bs, A.lay, bc.L);
+  if (threadIdx.x < (unsigned)bc.L) {
+    const int j = threadIdx.x;
+    SlabC c;
+    c.invS = bc.invS[j];
+    c.padS = bc.padS[j];
+    c.A0 = bc.A[j];
+    c.B0 = bc.B[j];
+    c.A1 = bc.A[j + 1];
+    c.B1 = bc.B[j + 1];
+    c.invS1 = bc.invS[j + 1];
+    c.start = A.lay->start[j];
+    c.nj = A.lay->start[j + 1] - c.start;
+    c.off = A.lay->dir_off[j];
+    c.sh = A.lay->shift[j];
+    scs[j] = c;
+  }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpSm& sm = sm_all[wid];
-  const uint32_t g = blockIdx.x * QK_WARPS + wid;  // light warp id
+  const int lane = threadIdx.x & 31;
+  const uint32_t g = blockIdx.x * QK_WARPS + (threadIdx.x >> 5);  // light warp
   const uint32_t nlight = A.n - A.lay->heavy_end;
-  const uint32_t idx = g * 32u + lane;
   if (g * 32u >= nlight) return;
+  const uint32_t idx = g * 32u + lane;
   const bool valid = idx < nlight;
   const uint32_t k = valid ? __ldg(A.order + idx) : 0u;
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
-  const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t le = (2u << lane) - 1u;  // lanes <= lane (lane 31: 2u << 31 == 0 -> all)
+  const uint64_t keep = policy_keep();
+  const double T4 = bc.T4;
 
   uint32_t qkey = 0, qid = 0;
   if (valid) {
-    qkey = A.skey[k];
-    qid = A.sid[k];
+    qkey = __ldg(A.skey + k);
+    qid = __ldg(A.sid + k);
   }
   const uint32_t qband = qkey >> kBandShift;
   const I qq = (I)(qkey & kQMask);
   PointRec q;
   q.theta = 0.0; q.s = 1.0; q.a = 1.0; q.b = 1.0;
   if (valid) q = A.pts[k + bs.start[qband]];  // first copy of the doubled slab
-  const double qinv4s = 0.25 / q.s;
-  sm.qA[lane] = make_double2(q.theta, 4.0 * q.s);
-  sm.qB[lane] = make_double2(q.a, q.b);
-  unsigned long long cur = 0;  // count: degree; emit: next row slot
-  if (MODE != QM_COUNT && valid) cur = A.offs[qid];
-  __syncwarp();
+  const double qinv4s = inv4s_of(q.s);
+  const double q4s = 4.0 * q.s;
 
-  // candidate-bit chain (count writes, emit replays)
-  uint32_t blk = NO_BLOCK, t32 = 0, myword = 0;
-  bool bits_ok = (MODE == QM_COUNT) && (A.bits != nullptr);
-  if (MODE == QM_EMIT_BITS) {
-    blk = A.warp_first[g];
-    if (blk != NO_BLOCK) myword = A.bits[(uint64_t)blk * 32u + lane];
+  RowWriter<FMT> rw;
+  if (MODE != QM_COUNT) {
+    rw.stage = stage_all + threadIdx.x * kStageStride;
+    rw.pos = rw.start = valid ? A.offs[qid] : 0ull;
   }
-  auto flush_bits = [&]() {
-    uint32_t nb = NO_BLOCK;
-    if (lane == 0) {
-      const uint32_t sub = g & (kBitSubPools - 1);
-      const uint32_t idx = atomicAdd(&A.pool_cursor[sub], 1u);
-      if (idx < A.pool_sub_blocks) nb = sub * A.pool_sub_blocks + idx;
-    }
-    nb = __shfl_sync(FULL, nb, 0);
-    if (nb == NO_BLOCK) {
-      bits_ok = false;
-      if (lane == 0) atomicOr(&A.sc->bit_overflow, 1u);
-      return;
-    }
-    if (lane == 0) {
-      A.bit_next[nb] = NO_BLOCK;  // chain terminator (the emit pass reads one link ahead)
-      if (blk == NO_BLOCK) A.warp_first[g] = nb;
-      else A.bit_next[blk] = nb;
-    }
-    A.bits[(uint64_t)nb * 32u + lane] = myword;
-    blk = nb;
-  };
+  uint32_t deg = 0;           // count pass
+  uint32_t bitpos = 0, word = 0;
+  uint32_t* const wbits = A.bits + (uint64_t)g * (kLightBitRows * 32u) + lane;
+  bool retest = MODE == QM_EMIT;
+  if (MODE == QM_EMIT_BITS) retest = A.warp_over[g] != 0;
+  bool over = false;          // count: some lane ran out of bit words
+  unsigned long long tested = 0, certain = 0;
 
-  unsigned long long tested = 0, certain = 0;  // count-pass statistics (warp-uniform)
   int jlo = 0;
   if (outward) jlo = (int)__reduce_min_sync(FULL, valid ? qband : 0xffffu);
-  const double T4 = bc.T4;
-
-  // window numerator T4 - 4 sinh^2((r_v - c)/2) at c = c_j, carried from slab to slab
-  double num_j;
-  {
-    const double h0 = __fma_rn(q.a, bc.B[jlo], -__dmul_rn(q.b, bc.A[jlo]));
-    num_j = __fma_rn(-h0, h0, T4);
-  }
   for (int j = jlo; j < bc.L; ++j) {
-    const double h1 = __fma_rn(q.a, bc.B[j + 1], -__dmul_rn(q.b, bc.A[j + 1]));
-    const double num_j1 = __fma_rn(-h1, h1, T4);
-    const double num_here = num_j;
-    num_j = num_j1;
-    const uint32_t bstart = bs.start[j];
-    const uint32_t nj = bs.start[j + 1] - bstart;
+    const SlabC& S = scs[j];
+    const uint32_t nj = S.nj;
     if (nj == 0) continue;
-    const uint32_t gbase = 2u * bstart;  // doubled segment of slab j
+    const uint32_t bstart = S.start, gbase = 2u * bstart;
     const bool on = valid && (!outward || j >= (int)qband);
     SlabWin<I> w;
     w.a = w.b = w.h0 = w.h1 = w.cs = w.ce = 0;
-    if (on) slab_window<I>(j, bc, bs, qq, num_here, num_j1, qinv4s, A.dir, w);
+    if (on) {
+      const double h0 = __fma_rn(q.a, S.B0, -__dmul_rn(q.b, S.A0));
+      const double h1 = __fma_rn(q.a, S.B1, -__dmul_rn(q.b, S.A1));
+      const double num0 = __fma_rn(-h0, h0, T4), num1 = __fma_rn(-h1, h1, T4);
+      if (WIDE) {
+        slab_window<I>(j, bc, bs, qq, num0, num1, qinv4s, A.dir, w);
+      } else {
+        SlabWin<int32_t> w32;
+        win32(S, (int32_t)qq, num0, num1, qinv4s, bc.T4min, A.dir, w32);
+        w.a = w32.a; w.b = w32.b; w.h0 = w32.h0; w.h1 = w32.h1; w.cs = w32.cs; w.ce = w32.ce;
+      }
+    }
     const bool own = on && (j == (int)qband);
-    const bool anyown = __any_sync(FULL, own);  // warp-uniform: only near slab boundaries / own slab
     I e1 = 0, wx = 0;
     if (own) {
       const I kv = (I)(k - bstart);
       if (outward) { e1 = 0; wx = kv + 1; } else { e1 = kv; wx = 1; }
     }
-    // certain pieces
-    I clo[2] = {w.cs, 0}, cln[2] = {w.ce - w.cs, 0};
-    if (own) cut_piece<I>(w.cs, w.ce, e1, wx, (I)nj, clo[0], cln[0], clo[1], cln[1]);
-    const uint32_t ct = (uint32_t)(cln[0] + cln[1]);
+    // certain pieces (own slab: minus v itself / minus the partners sorted before v)
+    I clo0 = w.cs, cln0 = w.ce - w.cs, clo1 = 0, cln1 = 0;
+    if (own) cut_piece<I>(w.cs, w.ce, e1, wx, (I)nj, clo0, cln0, clo1, cln1);
+    const uint32_t ct = (uint32_t)(cln0 + cln1);
     const uint32_t nt = (uint32_t)((w.b - w.a) - (w.h1 - w.h0));
-
     if (MODE == QM_COUNT) {
-      cur += ct;
+      deg += ct;
       certain += ct;
     } else {
-      // ---- certain edges: flattened copy of the 32 lanes' pieces ----
-      const uint32_t cinc = warp_incl(ct);
-      const uint32_t ctot = __shfl_sync(FULL, cinc, 31);
-      if (ctot) {
-        const uint32_t cex = cinc - ct;
-        const uint32_t NEc = __ballot_sync(FULL, ct > 0);
-        if (ct > 0) {
-          CRec c;
-          c.src0 = gbase + (uint32_t)clo[0] - cex;
-          c.thr = cex + (uint32_t)cln[0];
-          c.src1 = gbase + (uint32_t)clo[1] - cex - (uint32_t)cln[0];
-          c.vid = qid;
-          c.dst = cur - cex;
-          c.pad = 0;
-          sm.cr[__popc(NEc & lt)] = c;
-        }
-        __syncwarp();
-        int R0 = -1;
-        for (uint32_t t0 = 0; t0 < ctot; t0 += 32) {
-          const uint32_t t = t0 + lane;
-          const uint32_t s = cex - t0;
-          const uint32_t bit = (ct > 0 && s < 32u) ? (1u << s) : 0u;
-          const uint32_t M = __reduce_or_sync(FULL, bit);
-          const int r = R0 + __popc(M & le);
-          if (t < ctot) {
-            const CRec c = sm.cr[r];
-            const uint32_t src = (t < c.thr ? c.src0 : c.src1) + t;
-            write_edge<FMT>(A, c.dst + t, c.vid, __ldg(A.sid2 + src));
-          }
-          R0 += __popc(M);
-        }
-        cur += ct;
-        __syncwarp();
-      }
-    }
-
-    // ---- annulus candidates: flattened exact tests ----
-    const uint32_t tinc = warp_incl(nt);
-    const uint32_t tot = __shfl_sync(FULL, tinc, 31);
-    if (tot == 0) continue;
-    const uint32_t tex = tinc - nt;
-    {
-      const uint32_t NE = __ballot_sync(FULL, nt > 0);
-      if (nt > 0) {
-        QRec rc;
-        rc.aoff = gbase + (uint32_t)w.a - tex;
-        rc.thr = tex + (uint32_t)(w.h0 - w.a);
-        rc.hlen = (uint32_t)(w.h1 - w.h0);
-        rc.lane = (uint32_t)lane;
-        const int rk = __popc(NE & lt);
-        sm.rec[rk] = rc;
-        if (anyown) {
-          XRec x;
-          x.e1 = gbase + (uint32_t)e1;
-          x.e2 = gbase + (uint32_t)e1 + nj;
-          x.w = (uint32_t)wx;
-          x.pad = 0;
-          sm.xr[rk] = x;
+      // ---- certain edges: copy the ids into my row, 4 aligned ids per load ----
+      const uint32_t c0 = gbase + (uint32_t)clo0, c1 = gbase + (uint32_t)clo1;
+      const uint32_t l0 = (uint32_t)cln0, l1 = (uint32_t)cln1;
+      const uint32_t a0 = c0 & ~3u, a1 = c1 & ~3u;
+      const uint32_t n0 = l0 ? (c0 + l0 - a0 + 3u) >> 2 : 0u;
+      const uint32_t n1 = l1 ? (c1 + l1 - a1 + 3u) >> 2 : 0u;
+      const uint32_t nit = n0 + n1;
+      const uint32_t mc = __reduce_max_sync(FULL, nit);
+      for (uint32_t i = 0; i < mc; ++i) {
+        if (i < nit) {
+          const bool second = i >= n0;
+          const uint32_t c = second ? c1 : c0, l = second ? l1 : l0;
+          const uint32_t x = (second ? a1 + 4u * (i - n0) : a0 + 4u * i);
+          const uint4 v = ld4_keep(A.sid2 + x, keep);
+          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+          const uint32_t lo = c > x ? c - x : 0u;
+          const uint32_t hi = min(c + l - x, 4u);
+          rw.put4(A, qid, wv, lo, hi);
         }
       }
     }
-    __syncwarp();
-    if (MODE == QM_COUNT) tested += tot;
-    int R0 = -1;
-    for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
-      const uint32_t t = t0 + lane;
-      bool act = t < tot;
-      const uint32_t s = tex - t0;
-      const uint32_t bit = (nt > 0 && s < 32u) ? (1u << s) : 0u;
-      const uint32_t M = __reduce_or_sync(FULL, bit);
-      const int r = R0 + __popc(M & le);
-      R0 += __popc(M);
-      const QRec rc = sm.rec[r];
-      const uint32_t p = rc.aoff + t + (t >= rc.thr ? rc.hlen : 0u);
-      uint32_t hm;
-      if (MODE == QM_EMIT_BITS) {
-        hm = __shfl_sync(FULL, myword, t32);
+    // ---- annulus: exact tests ----
+    const uint32_t mt = __reduce_max_sync(FULL, nt);
+    if (mt == 0) continue;
+    const uint32_t pa = gbase + (uint32_t)w.a, thr = (uint32_t)(w.h0 - w.a);
+    const uint32_t hl = (uint32_t)(w.h1 - w.h0);
+    // own-slab exclusion in doubled positions: [x1, x1 + wx) and [x1 + nj, ...)
+    const uint32_t x1 = gbase + (uint32_t)e1, xw = (uint32_t)wx;
+    if (MODE == QM_COUNT) tested += nt;
+    for (uint32_t i = 0; i < mt; ++i) {
+      const bool act = i < nt;
+      const uint32_t p = pa + i + (i >= thr ? hl : 0u);
+      bool hit;
+      if (MODE == QM_EMIT_BITS && !retest) {
+        if ((bitpos & 31u) == 0) word = wbits[(bitpos >> 5) * 32u];
+        hit = act && ((word >> (bitpos & 31u)) & 1u);
       } else {
-        if (anyown) {
-          const XRec x = sm.xr[r];
-          act = act && !((p - x.e1) < x.w || (p - x.e2) < x.w);
-        }
-        const double2* pp = reinterpret_cast<const double2*>(A.pts + (act ? p : 0u));
-        const double2 w0 = __ldg(pp), w1 = __ldg(pp + 1);  // (theta, s), (a, b)
-        const double2 qa_ = sm.qA[rc.lane], qb_ = sm.qB[rc.lane];
-        hm = __ballot_sync(FULL, certified_edge(qa_.x, qa_.y, qb_.x, qb_.y, w0, w1, T4, act));
+        const bool ex = (p - x1) < xw || (p - x1 - nj) < xw;
+        const bool tst = act && !ex;
+        uint32_t r[8];
+        const PointRec* wp = A.pts + (tst ? p : 0u);
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                       "=r"(r[6]), "=r"(r[7])
+                     : "l"(wp));
+        const double2 w0 = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+        const double2 w1 = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
+        hit = certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, tst);
       }
-      // my own candidates in this batch: lanes [tex - t0, tex + nt - t0) of the batch
-      const int lo = max((int)tex - (int)t0, 0), hi = min((int)(tex + nt) - (int)t0, 32);
-      const uint32_t mine = __popc(hm & lane_range_mask(lo, hi));
       if (MODE == QM_COUNT) {
-        cur += mine;
-        if (bits_ok) {
-          if (lane == (int)t32) myword = hm;
-          if (t32 == 31) flush_bits();
+        deg += hit;
+        if (act) {  // the word of a group is stored at the group's end and at slab ends
+          word |= (uint32_t)hit << (bitpos & 31u);
+          const bool full = (bitpos & 31u) == 31u;
+          if (full || i + 1 == nt) {
+            if ((bitpos >> 5) < kLightBitRows) wbits[(bitpos >> 5) * 32u] = word;
+            else over = true;
+          }
+          if (full) word = 0;
         }
-      } else {
-        const int o = (int)rc.lane;
-        const uint32_t olo = (uint32_t)__shfl_sync(FULL, lo, o);
-        const unsigned long long ocur = __shfl_sync(FULL, cur, o);
-        uint32_t ovid = 0;
-        if (FMT != RHG_CSR) ovid = __shfl_sync(FULL, qid, o);
-        if ((hm >> lane) & 1u)
-          write_edge<FMT>(A, ocur + __popc(hm & lt & ~((1u << olo) - 1u)), ovid,
-                          __ldg(A.sid2 + p));
-        cur += mine;
-        if (MODE == QM_EMIT_BITS && t32 == 31) {
-          blk = (blk != NO_BLOCK) ? A.bit_next[blk] : NO_BLOCK;
-          if (blk != NO_BLOCK) myword = A.bits[(uint64_t)blk * 32u + lane];
-        }
+      } else if (hit) {
+        rw.put(A, qid, ld_keep(A.sid2 + p, keep));
       }
-      t32 = (t32 + 1) & 31u;
+      if (act) ++bitpos;
     }
-    __syncwarp();
   }
   if (MODE == QM_COUNT) {
-    if (bits_ok && t32 != 0) flush_bits();
-    if (valid) A.deg[qid] = (uint32_t)cur;
+    if (valid) A.deg[qid] = deg;
+    const bool anyover = __any_sync(FULL, over);
+    if (lane == 0) {
+      A.warp_over[g] = anyover ? 1u : 0u;
+      if (anyover) atomicOr(&A.sc->bit_overflow, 1u);
+    }
+    tested = warp_incl(tested);
     certain = warp_incl(certain);
     if (lane == 31) {
       atomicAdd(&A.sc->candidates, tested);
       atomicAdd(&A.sc->certain, certain);
     }
+  } else if (valid) {
+    rw.finish(A);
   }
 }
 
@@ -580,15 +690,14 @@ __global__ void __launch_bounds__(HV_THREADS)
       }
     }
     // compact the lane's non-empty pieces (slab order, then piece order)
-    uint32_t cnt = 0, cand = 0, words = 0;
+    uint32_t cnt = 0, cand = 0;
 #pragma unroll
     for (int x = 0; x < 6; ++x) {
       cnt += ln[x] > 0;
       cand += (uint32_t)ln[x];
-      if (x < (int)kTestPieces) words += ((uint32_t)ln[x] + 31u) >> 5;
     }
-    const uint32_t ci = warp_incl(cnt), ca = warp_incl(cand), cw = warp_incl(words);
-    uint32_t slot = i * LS + (ci - cnt), off = ca - cand, woff = cw - words;
+    const uint32_t ci = warp_incl(cnt), ca = warp_incl(cand);
+    uint32_t slot = i * LS + (ci - cnt), off = ca - cand;
 #pragma unroll
     for (int x = 0; x < 6; ++x) {
       if (ln[x] > 0) {
@@ -596,16 +705,13 @@ __global__ void __launch_bounds__(HV_THREADS)
         H.pstart[slot] = gbase + (uint32_t)lo[x];
         H.plen[slot] = len | (x < (int)kTestPieces ? 0u : kCertainPiece);
         H.poff[slot] = off;
-        H.pword[slot] = woff;
         ++slot;
         off += len;
-        if (x < (int)kTestPieces) woff += (len + 31u) >> 5;
       }
     }
     if (lane == 31) {
       H.np[i] = ci;
       H.vtot[i] = ca;
-      H.vwords[i] = cw;
     }
     if (lane == 0) A.deg[A.sid[i]] = 0u;
   }
@@ -618,7 +724,6 @@ __global__ void k_heavy_chunk_size(const HeavyArgs H) {
   if (ch < H.chunk_min) ch = H.chunk_min;
   ch = (ch + 31ull) & ~31ull;  // whole 32-candidate groups
   H.meta->chunk = ch;
-  H.meta->bits_overflow = (H.meta->words > H.bits_cap) ? 1u : 0u;
 }
 
 __global__ void k_heavy_chunk_counts(const HeavyArgs H) {
@@ -653,22 +758,32 @@ __global__ void __launch_bounds__(HV_THREADS) k_heavy_chunk_map(const HeavyArgs 
   }
 }
 
+// One warp per chunk: [lo, hi) of hub vertex i's candidate sequence (the
+// concatenation of its pieces).  The warp holds up to 32 of the chunk's pieces in
+// registers (one per lane) and walks the chunk 32 candidates per batch; the piece
+// of candidate t is found like the light kernel's owner (OR of segment-start bits
+// + popcount).  Certain pieces count as hits without a test.  Ballot words are
+// stored per chunk (CH / 32 + 8 words per chunk) for the emit pass to replay.
 template <int MODE, int FMT>
-__global__ void __launch_bounds__(HV_THREADS)
+__global__ void __launch_bounds__(HV_THREADS, 4)
     k_heavy(const QueryArgs A, const HeavyArgs H, const __grid_constant__ BandConst bc) {
   const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
   const unsigned long long gw = blockIdx.x * HV_WARPS + (threadIdx.x >> 5);
   const unsigned long long TW = (unsigned long long)gridDim.x * HV_WARPS;
   const unsigned long long nch = H.meta->nchunks, CH = H.meta->chunk;
   const uint32_t LS = kRangesPerSlab * (uint32_t)bc.L;
   const double T4 = bc.T4;
-  const bool bits = !H.meta->bits_overflow;
+  const unsigned long long WPC = (CH >> 5) + 8;  // bit words per chunk (+ window seams)
+  const bool bits = nch * WPC <= H.bits_cap;
+  const uint64_t keep = policy_keep();
   unsigned long long cand_total = 0, cert_total = 0;
   for (unsigned long long c = gw; c < nch; c += TW) {
     const uint32_t i = H.chunk_vtx[c];
     const unsigned long long c0 = H.choff[i];
-    const unsigned long long lo = (c - c0) * CH, hi = lo + CH;
+    const uint32_t lo = (uint32_t)((c - c0) * CH);
+    const uint32_t vt = H.vtot[i];
+    const uint32_t hi = (uint32_t)min((unsigned long long)vt, (unsigned long long)lo + CH);
     const uint32_t np = H.np[i];
     const uint32_t qid = A.sid[i];
     unsigned long long base = 0;
@@ -676,79 +791,65 @@ __global__ void __launch_bounds__(HV_THREADS)
     const uint32_t qband = A.skey[i] >> kBandShift;
     const PointRec q = A.pts[i + A.lay->start[qband]];
     const double q4s = 4.0 * q.s;
-    const unsigned long long wb = H.vwbase[i];
-    uint32_t run = 0;
-    for (uint32_t pc = H.chunk_piece[c]; pc < np; ++pc) {
-      const uint64_t s = (uint64_t)i * LS + pc;
-      const unsigned long long off = H.poff[s];
-      if (off >= hi) break;
-      const uint32_t lf = H.plen[s];
-      const uint32_t len = lf & ~kCertainPiece;
-      const uint32_t st = H.pstart[s];
-      // groups k whose first candidate off + 32 k lies in [lo, hi)
-      const uint32_t k0 = off >= lo ? 0u : (uint32_t)((lo - off + 31) >> 5);
-      const uint32_t k1 = (uint32_t)min((unsigned long long)((len + 31u) >> 5), (hi - off + 31) >> 5);
-      if (lf & kCertainPiece) {  // every candidate is an edge
-        if (MODE == QM_COUNT) {
-          const uint32_t m = min(32u * k1, len) - min(32u * k0, len);
-          run += m;
-          cert_total += m;
-        } else {
-          for (uint32_t k = k0; k < k1; k += 4) {  // 4 groups of loads in flight
-            uint32_t w[4];
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint32_t u = 32u * (k + g) + lane;
-              w[g] = (k + g < k1 && u < len) ? __ldg(A.sid2 + st + u) : 0u;
-            }
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint32_t u = 32u * (k + g) + lane;
-              if (k + g < k1 && u < len) write_edge<FMT>(A, base + run + lane, qid, w[g]);
-              if (k + g < k1) run += min(32u, len - 32u * (k + g));
-            }
-          }
-        }
-        continue;
+    const unsigned long long wbase = c * WPC;
+    uint32_t run = 0, bt = 0;  // hits so far, batch index within the chunk
+    uint32_t pc = H.chunk_piece[c];
+    uint32_t t0 = 0;           // chunk-relative candidate index of the next batch
+    const uint32_t span = hi - lo;
+    while (t0 < span) {
+      // ---- up to 32 pieces, one per lane, clipped to the chunk ----
+      const uint32_t mp = pc + lane;
+      uint32_t ps = 0, pe = 0, pst = 0, pcert = 0;
+      if (mp < np) {
+        const uint64_t sl = (uint64_t)i * LS + mp;
+        const uint32_t off = H.poff[sl], lf = H.plen[sl];
+        const uint32_t len = lf & ~kCertainPiece;
+        ps = max(off, lo) - lo;
+        pe = min(off + len, hi);
+        pe = pe > lo ? pe - lo : 0u;
+        pst = H.pstart[sl] + (lo > off ? lo - off : 0u) - ps;  // position = pst + t
+        pcert = lf & kCertainPiece;
       }
-      const unsigned long long wq = wb + H.pword[s];
-      for (uint32_t k = k0; k < k1; k += 4) {  // 4 groups of loads in flight
-        uint32_t m[4];
-        uint32_t pp[4];
+      // candidates [t0, wend) are covered by this group of pieces (pieces are
+      // contiguous and non-empty; pieces past the chunk end clip to empty)
+      const uint32_t pe31 = __shfl_sync(FULL, pe, 31);
+      const uint32_t wend = pc + 32 >= np ? span : pe31;
+      int R0 = -1;
+      for (; t0 < wend; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        const uint32_t sb = ps - t0;
+        const uint32_t bit = (mp < np && pe > ps && sb < 32u) ? (1u << sb) : 0u;
+        const uint32_t M = __reduce_or_sync(FULL, bit);
+        const int r = min(R0 + __popc(M & le), 31);
+        R0 += __popc(M);
+        const uint32_t o_st = __shfl_sync(FULL, pst, r);
+        const uint32_t o_cert = __shfl_sync(FULL, pcert, r);
+        const bool act = t < wend;
+        const uint32_t p = o_st + t;
+        uint32_t m;
         if (MODE == QM_EMIT_BITS && bits) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            pp[g] = st + 32u * (k + g) + lane;
-            m[g] = (k + g < k1) ? H.bits[wq + k + g] : 0u;
-          }
+          m = H.bits[wbase + bt];
         } else {
-          double2 w0[4], w1[4];
-          bool act[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint32_t u = 32u * (k + g) + lane;
-            act[g] = (k + g < k1) && u < len;
-            pp[g] = st + (act[g] ? u : 0u);
-            const double2* xp = reinterpret_cast<const double2*>(A.pts + pp[g]);
-            w0[g] = __ldg(xp);
-            w1[g] = __ldg(xp + 1);
-          }
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            m[g] = __ballot_sync(FULL, certified_edge(q.theta, q4s, q.a, q.b, w0[g], w1[g], T4, act[g]));
-          if (MODE == QM_COUNT && bits && lane < 4 && k + lane < k1) {
-            const uint32_t mine = lane == 0 ? m[0] : (lane == 1 ? m[1] : (lane == 2 ? m[2] : m[3]));
-            H.bits[wq + k + lane] = mine;
+          const bool test = act && !o_cert;
+          const double2* xp = reinterpret_cast<const double2*>(A.pts + (test ? p : 0u));
+          const double2 w0 = __ldg(xp), w1 = __ldg(xp + 1);
+          const bool e = certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, test);
+          m = __ballot_sync(FULL, e || (act && o_cert));
+          if (MODE == QM_COUNT && bits && lane == 0) H.bits[wbase + bt] = m;
+          if (MODE == QM_COUNT) {
+            const uint32_t na = __popc(__ballot_sync(FULL, act));
+            const uint32_t nc = __popc(__ballot_sync(FULL, act && o_cert));
+            cand_total += na - nc;
+            cert_total += nc;
           }
         }
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          if (MODE != QM_COUNT && ((m[g] >> lane) & 1u))
-            write_edge<FMT>(A, base + run + __popc(m[g] & lt), qid, __ldg(A.sid2 + pp[g]));
-          run += __popc(m[g]);
-          if (MODE == QM_COUNT && k + g < k1) cand_total += min(32u, len - 32u * (k + g));
-        }
+        if (MODE != QM_COUNT && ((m >> lane) & 1u))
+          write_edge<FMT>(A, base + run + __popc(m & lt), qid, ld_keep(A.sid2 + p, keep));
+        run += __popc(m);
+        ++bt;
       }
+      t0 = wend;
+      pc += 32;
     }
     if (MODE == QM_COUNT && lane == 0) {
       H.chunk_hits[c] = run;
@@ -770,9 +871,6 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
   else k_heavy_ranges<RHG_EDGES_UNDIRECTED><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);
   cudaError_t e = exclusive_scan_u32_u64_dev(ha.vcap, &ha.meta->nvtx, ha.vtot, ha.vtot_off,
                                              scan_tmp, &ha.meta->cand, st, launches);
-  if (e != cudaSuccess) return e;
-  e = exclusive_scan_u32_u64_dev(ha.vcap, &ha.meta->nvtx, ha.vwords, ha.vwbase, scan_tmp,
-                                 &ha.meta->words, st, launches);
   if (e != cudaSuccess) return e;
   k_heavy_chunk_size<<<1, 1, 0, st>>>(ha);
   k_heavy_chunk_counts<<<148 * 4, 256, 0, st>>>(ha);
@@ -806,10 +904,10 @@ cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
   const bool wide = qa.n >= (1u << 30);  // a slab may hold >= 2^30 points: 64-bit positions
-#define RHG_LQ(M, F)                                                      \
-  do {                                                                    \
-    if (wide) k_query<M, F, true><<<blocks, QK_THREADS, 0, st>>>(qa, bc); \
-    else k_query<M, F, false><<<blocks, QK_THREADS, 0, st>>>(qa, bc);     \
+#define RHG_LQ(M, F)                                                                   \
+  do {                                                                                 \
+    if (wide) k_query<M, F, true><<<blocks, QK_THREADS, 0, st>>>(qa, bc);              \
+    else k_query<M, F, false><<<blocks, QK_THREADS, 0, st>>>(qa, bc);                  \
   } while (0)
   if (mode == QM_COUNT) {
     if (fmt == RHG_CSR) RHG_LQ(QM_COUNT, RHG_CSR);

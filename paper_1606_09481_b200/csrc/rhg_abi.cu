@@ -55,13 +55,18 @@ rhg_status target_radius(double n, double kbar, double alpha, double* R) {
   return RHG_OK;
 }
 
-// "log n" slabs (base unstated; Z7): ceil(ln n).  The
-// edge set does not depend on L; ln n measured faster than log2 n on B200 (fewer
-// window evaluations per vertex, slightly more tests).
+// Layout defaults (Z7): L <= 16 slabs with width ratio p = 0.85 (the
+// paper uses p = 0.9; with L capped at 16, 0.85 gives fewer tests).
+constexpr int kDefaultMaxBands = 16;
+constexpr double kDefaultBandRatio = 0.85;
+
+// "log n" slabs (base unstated; Z7): ceil(ln n), capped at
+// 16 so that one warp evaluates all windows of two vertices at once (k_query).
+// The edge set does not depend on L or p.
 int default_bands(uint64_t n) {
   int L = (int)std::ceil(std::log((double)n));
   if (L < 1) L = 1;
-  return L > kMaxBands ? kMaxBands : L;
+  return L > kDefaultMaxBands ? kDefaultMaxBands : L;
 }
 
 // Slab boundaries: c_0 = 0, c_1 = (1-p)R/(1-p^L),
@@ -84,7 +89,7 @@ uint64_t heavy_cap_for(uint64_t n) {
 
 rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandConst* bc) {
   int L = (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
-  double p = (opt && opt->band_ratio > 0.0) ? opt->band_ratio : 0.9;
+  double p = (opt && opt->band_ratio > 0.0) ? opt->band_ratio : kDefaultBandRatio;
   if (L < 1 || L > kMaxBands || !(p > 0.0 && p < 1.0)) return RHG_ERR_INVALID;
   memset(bc, 0, sizeof(*bc));
   bc->L = L;
@@ -110,10 +115,10 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, sid2, dir, deg, offs,
       scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
-  size_t h_pstart, h_plen, h_poff, h_pword, h_np, h_vtot, h_vwords, h_vtot_off, h_vwbase, h_cc,
+  size_t h_pstart, h_plen, h_poff, h_np, h_vtot, h_vtot_off, h_cc,
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
-  size_t b_pool, b_next, b_first, b_cursor, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
-  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, pool_blocks, pool_sub_blocks, light_warps;
+  size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
+  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps;
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
@@ -130,14 +135,11 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.vcap = heavy_cap_for(n);
   L.nslots_cap = L.vcap * (uint64_t)kRangesPerSlab * (uint64_t)nbands;
   L.chunk_cap = L.vcap + kChunkExtra;
-  // Candidate bits (emit replays them instead of re-testing).  Expected tests:
-  // ~1.14 per directed CSR entry, ~1.2 per undirected edge (outward scan); sized
-  // with margin from the output capacity.  Overflow falls back to re-testing.
+  // Hub ballot words (k_heavy) are sized from the output capacity (~1.1-1.4 tests
+  // per directed CSR entry); light warps get kLightBitRows x 32 words each.
   const uint64_t cap_tests = (f == RHG_CSR) ? cap + cap / 2 : 2 * cap;
   L.light_warps = (n + 31) / 32;
-  L.pool_sub_blocks = (cap_tests / 1024 + L.light_warps + 64 * 16) / kBitSubPools + 1;
-  L.pool_blocks = L.pool_sub_blocks * kBitSubPools;
-  L.hbits_cap = cap_tests / 64 + L.nslots_cap / 2 + 1024;
+  L.hbits_cap = cap_tests / 32 + L.vcap * 48 + 1024;  // >= nchunks (CH/32 + 8) when hubs fit
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -168,12 +170,9 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.h_pstart = take(4 * L.nslots_cap);
   L.h_plen = take(4 * L.nslots_cap);
   L.h_poff = take(4 * L.nslots_cap);
-  L.h_pword = take(4 * L.nslots_cap);
   L.h_np = take(4 * L.vcap);
   L.h_vtot = take(4 * L.vcap);
-  L.h_vwords = take(4 * L.vcap);
   L.h_vtot_off = take(8 * (L.vcap + 1));
-  L.h_vwbase = take(8 * (L.vcap + 1));
   L.h_cc = take(4 * L.vcap);
   L.h_choff = take(8 * (L.vcap + 1));
   L.h_cvtx = take(4 * L.chunk_cap);
@@ -181,10 +180,8 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.h_chits = take(4 * L.chunk_cap);
   L.h_cpos = take(8 * (L.chunk_cap + 1));
   L.h_bits = take(4 * L.hbits_cap);
-  L.b_pool = take(128 * L.pool_blocks);
-  L.b_next = take(4 * L.pool_blocks);
-  L.b_first = take(4 * L.light_warps);
-  L.b_cursor = take(4 * kBitSubPools);
+  L.b_bits = take(4ull * kLightBitRows * 32 * L.light_warps);
+  L.b_over = take(4 * L.light_warps);
   L.q_order = take(4 * n);
   L.q_cell_lo = take(4 * kQuerySectors * kMaxBands);
   L.q_cell_cnt = take(4 * kQuerySectors * kMaxBands);
@@ -264,6 +261,8 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   const int host = out->host_buffers ? 1 : 0;
   if (f == RHG_CSR && (!out->row_ptr || (!out->col && out->capacity_edges))) return RHG_ERR_INVALID;
   if (f == RHG_EDGES_UNDIRECTED && !out->pairs && out->capacity_edges) return RHG_ERR_INVALID;
+  // device outputs are written in whole 32-byte sectors (k_query): 32-byte alignment
+  if (!host && (((uintptr_t)out->col | (uintptr_t)out->pairs) & 31)) return RHG_ERR_INVALID;
   if (!sample && (!theta_in || !r_in)) return RHG_ERR_INVALID;
   BandConst bc;
   rhg_status s = make_band_const(n, R, out->options, &bc);
@@ -356,25 +355,17 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.dir = dir;
   qa.lay = lay;
   qa.order = (const uint32_t*)(ws + Lw.q_order);
-  qa.bits = (uint32_t*)(ws + Lw.b_pool);
-  qa.bit_next = (uint32_t*)(ws + Lw.b_next);
-  qa.warp_first = (uint32_t*)(ws + Lw.b_first);
-  qa.pool_cursor = (uint32_t*)(ws + Lw.b_cursor);
-  qa.pool_sub_blocks = (uint32_t)Lw.pool_sub_blocks;
-  CK(cudaMemsetAsync(qa.pool_cursor, 0, 4 * kBitSubPools, st));
-  CK(cudaMemsetAsync(qa.warp_first, 0xff, 4 * Lw.light_warps, st));
+  qa.bits = (uint32_t*)(ws + Lw.b_bits);
+  qa.warp_over = (uint32_t*)(ws + Lw.b_over);
   qa.deg = deg;
   qa.sc = sc;
   HeavyArgs ha{};
   ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
   ha.plen = (uint32_t*)(ws + Lw.h_plen);
   ha.poff = (uint32_t*)(ws + Lw.h_poff);
-  ha.pword = (uint32_t*)(ws + Lw.h_pword);
   ha.np = (uint32_t*)(ws + Lw.h_np);
   ha.vtot = (uint32_t*)(ws + Lw.h_vtot);
-  ha.vwords = (uint32_t*)(ws + Lw.h_vwords);
   ha.vtot_off = (uint64_t*)(ws + Lw.h_vtot_off);
-  ha.vwbase = (uint64_t*)(ws + Lw.h_vwbase);
   ha.cc = (uint32_t*)(ws + Lw.h_cc);
   ha.choff = (uint64_t*)(ws + Lw.h_choff);
   ha.chunk_vtx = (uint32_t*)(ws + Lw.h_cvtx);
@@ -408,10 +399,10 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.offs = offs;
   qa.col = col_dev;
   qa.pairs = pairs_dev;
-  // hub chunks replay their bits unless the hub bit buffer overflowed (checked on
-  // the device); light warps replay theirs unless a sub-pool ran dry.
+  // hub chunks replay their bits unless the hub bit buffer was too small (checked
+  // on the device); light warps replay theirs unless they ran out of bit words.
   CK(launch_heavy(QM_EMIT_BITS, f, qa, ha, bc, st));
-  CK(launch_query(hs.bit_overflow ? QM_EMIT : QM_EMIT_BITS, f, qa, bc, st));
+  CK(launch_query(QM_EMIT_BITS, f, qa, bc, st));  // warps whose bits overflowed re-test
   launches += 2;
   tm.mark();  // 6
   if (host) {

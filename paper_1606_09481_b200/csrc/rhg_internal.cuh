@@ -13,7 +13,7 @@ constexpr int kBandShift = 27;         // sort key = band << 27 | q27(theta)
 constexpr uint32_t kQBits = 27;
 constexpr uint32_t kQMax = (1u << kQBits) - 1u;
 constexpr uint32_t kQMask = kQMax;
-constexpr uint32_t kBitSubPools = 64;
+constexpr uint32_t kLightBitRows = 8;   // bit words per lane of a light warp (256 tests)
 constexpr int kQuerySectorBits = 8;    // light queries run sector-major over 2^8 angular sectors
 constexpr int kQuerySectors = 1 << kQuerySectorBits;  // light-warp bit blocks come from 64 sub-pools
 constexpr uint32_t kRangesPerSlab = 6;  // hub slots per (vertex, slab): 4 pieces to test + 2 certain
@@ -60,8 +60,6 @@ struct HeavyMeta {
   unsigned long long nchunks;  // total chunks
   unsigned long long chunk;    // chunk size (candidates, multiple of 32)
   unsigned long long hits;     // total edges of hub vertices (directed / outward)
-  unsigned long long words;    // candidate-bit words of the tested pieces
-  unsigned int bits_overflow;  // words > bits_cap: the hub emit re-tests
 };
 
 constexpr uint32_t kCertainPiece = 0x80000000u;  // plen flag: every candidate is an edge
@@ -71,19 +69,17 @@ struct HeavyArgs {
   uint32_t* pstart;         // first doubled position of the piece
   uint32_t* plen;           // candidates | kCertainPiece
   uint32_t* poff;           // offset of the piece in the vertex's candidate sequence
-  uint32_t* pword;          // offset of the piece's bit words in the vertex's words
   uint32_t* np;             // [vcap] pieces
   uint32_t* vtot;           // [vcap] candidates
-  uint32_t* vwords;         // [vcap] bit words
   uint64_t* vtot_off;       // [vcap + 1] scan of vtot (total -> meta->cand)
-  uint64_t* vwbase;         // [vcap + 1] scan of vwords
   uint32_t* cc;             // [vcap] chunks per vertex
   uint64_t* choff;          // [vcap + 1] scan of cc
   uint32_t* chunk_vtx;      // [chunk_cap]
   uint32_t* chunk_piece;    // [chunk_cap] first piece the chunk touches
   uint32_t* chunk_hits;     // [chunk_cap]
   uint64_t* chunk_pos;      // [chunk_cap + 1] scan of chunk_hits
-  uint32_t* bits;           // [bits_cap] hub candidate bits
+  uint32_t* bits;           // [bits_cap] hub ballot words, (CH / 32 + 8) per chunk; if they do
+                            // not fit, both passes test (same output)
   uint64_t bits_cap;
   HeavyMeta* meta;
   uint64_t vcap;
@@ -119,11 +115,8 @@ struct QueryArgs {
   const uint64_t* __restrict__ offs;  // emit pass: output offset per vertex id
   uint32_t* col;                      // CSR output
   uint32_t* pairs;                    // undirected output
-  uint32_t* bits;                     // light candidate bits: pool of 32-word blocks (or nullptr)
-  uint32_t* bit_next;                 // next block of a warp's chain
-  uint32_t* warp_first;               // first block of each light warp
-  uint32_t* pool_cursor;              // [kBitSubPools] allocation cursors
-  uint32_t pool_sub_blocks;           // blocks per sub-pool
+  uint32_t* bits;                     // light test bits: kLightBitRows x 32 words per light warp
+  uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
 };
 

@@ -51,8 +51,9 @@ def test_band_boundaries(rhg, orc):
     for n, R in [(10_000, 16.7), (10_000_000, 24.9), (100_000_000, 33.9)]:
         c = rhg.band_boundaries(n, R)
         L = len(c) - 1
-        assert L == int(np.ceil(np.log(n)))
-        assert np.allclose(c, orc.boundaries(R, L, 0.9), rtol=1e-12, atol=1e-12)
+        # default layout (Z7): L = min(16, ceil(ln n)), p = 0.85
+        assert L == min(16, int(np.ceil(np.log(n))))
+        assert np.allclose(c, orc.boundaries(R, L, 0.85), rtol=1e-12, atol=1e-12)
 
 
 def test_invalid_arguments_rejected_on_host(rhg):
