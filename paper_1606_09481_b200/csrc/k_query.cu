@@ -409,15 +409,16 @@ struct RowWriter {
       write_elems(A, s0, r, (uint32_t)(start - s0), EPS);
     }
   }
-  // append w[lo..hi) (hi - lo <= 4)
+  // append w[lo..hi) (hi - lo <= 4 < 2 EPS)
   __device__ __forceinline__ void put4(const QueryArgs& A, uint32_t vid, const uint32_t* w,
                                        uint32_t lo, uint32_t hi) {
+    const uint32_t p0 = (uint32_t)pos;  // ring arithmetic on the low bits
 #pragma unroll
     for (uint32_t u = 0; u < 4; ++u)
-      if (u >= lo && u < hi) store_elem((uint32_t)(pos + (u - lo)) & (2 * EPS - 1), vid, w[u]);
-    const unsigned long long old = pos;
+      if (u >= lo && u < hi) store_elem((p0 + u - lo) & (2 * EPS - 1), vid, w[u]);
+    const uint32_t p1 = p0 + (hi - lo);
     pos += hi - lo;
-    if ((old / EPS) != (pos / EPS)) flush(A, old / EPS);  // a sector completed
+    if ((p0 ^ p1) & ~(EPS - 1)) flush(A, (pos - (hi - lo)) / EPS);  // a sector completed
   }
   __device__ __forceinline__ void put(const QueryArgs& A, uint32_t vid, uint32_t w) {
     store_elem((uint32_t)pos & (2 * EPS - 1), vid, w);
@@ -579,6 +580,32 @@ __global__ void __launch_bounds__(QK_THREADS)
     // own-slab exclusion in doubled positions: [x1, x1 + wx) and [x1 + nj, ...)
     const uint32_t x1 = gbase + (uint32_t)e1, xw = (uint32_t)wx;
     if (MODE == QM_COUNT) tested += nt;
+    if (MODE == QM_EMIT_BITS && !retest) {
+      // replay: walk only the set bits of my words covering [bitpos, bitpos + nt)
+      const uint32_t bp0 = bitpos, bp1 = bitpos + nt;
+      const uint32_t wlo = bp0 >> 5, nw = nt ? ((bp1 + 31u) >> 5) - wlo : 0u;
+      const uint32_t mw = __reduce_max_sync(FULL, nw);
+      for (uint32_t u = 0; u < mw; ++u) {
+        uint32_t m = 0;
+        const uint32_t wb = (wlo + u) << 5;  // first bit position of this word
+        if (u < nw) {
+          m = wbits[(wlo + u) * 32u];
+          if (wb < bp0) m &= ~0u << (bp0 - wb);
+          if (bp1 - wb < 32u) m &= (1u << (bp1 - wb)) - 1u;
+        }
+        const uint32_t mh = __reduce_max_sync(FULL, (uint32_t)__popc(m));
+        for (uint32_t h = 0; h < mh; ++h) {
+          if (m) {
+            const uint32_t i = wb + (uint32_t)(__ffs(m) - 1) - bp0;
+            m &= m - 1u;
+            const uint32_t p = pa + i + (i >= thr ? hl : 0u);
+            rw.put(A, qid, ld_keep(A.sid2 + p, keep));
+          }
+        }
+      }
+      bitpos = bp1;
+      continue;
+    }
     for (uint32_t i = 0; i < mt; ++i) {
       const bool act = i < nt;
       const uint32_t p = pa + i + (i >= thr ? hl : 0u);
