@@ -180,6 +180,30 @@ def test_edge_cases(rhg, orc):
     assert rhg.generate_from_points(*_cpu_pts(th, r), R, "csr").num_edges == 50 * 49  # all coincide
 
 
+def test_clustered_angles(rhg, orc):
+    """Clustered angles: thousands of points in one directory bucket range and in
+    one sort digit; the edge set must match the oracle and must not depend on
+    the input order of the points."""
+    rng = np.random.default_rng(11)
+    R = 20.0
+    th = np.concatenate([1.0 + rng.uniform(0, 1e-3, 5000), rng.uniform(0, 2 * np.pi, 7000)])
+    r = np.concatenate([rng.uniform(R - 1, R, 5000), orc.sample_points(7000, 1.0, R, 5)[1]])
+    es = orc.brute_force(th, r, R)
+    for fmt in ("csr", "pairs"):
+        g = rhg.generate_from_points(*_cpu_pts(th, r), R, fmt)
+        compare_sets(csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g), es)
+    # same point set, shuffled ids: the same graph under the permutation
+    perm = rng.permutation(len(th))
+    g1 = rhg.generate_from_points(*_cpu_pts(th, r), R, "csr")
+    g2 = rhg.generate_from_points(*_cpu_pts(th[perm], r[perm]), R, "csr")
+    a = csr_checked_pairs(g1)
+    b = csr_checked_pairs(g2)
+    pm = perm.astype(np.uint64)  # vertex x of g2 is point perm[x] of g1
+    u, v = pm[(b >> np.uint64(32)).astype(np.int64)], pm[(b & np.uint64(0xffffffff)).astype(np.int64)]
+    b2 = np.sort((np.minimum(u, v) << np.uint64(32)) | np.maximum(u, v))
+    assert np.array_equal(a, b2)
+
+
 def test_ragged_sizes(rhg, orc):
     """Sizes that are not multiples of warps / tiles / sort blocks."""
     for n in (2, 3, 31, 33, 4095, 4097, 8193):
