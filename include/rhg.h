@@ -158,6 +158,9 @@ const char *rhg_status_string(rhg_status s);
 /* Library version string (build id). */
 const char *rhg_version(void);
 
+/* Text of the CUDA error behind the calling thread's last RHG_ERR_CUDA. */
+const char *rhg_last_cuda_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,7 @@ FORMATS = {"csr": RHG_CSR, "edges": RHG_EDGES_UNDIRECTED, "pairs": RHG_EDGES_UND
 # Symbols include/rhg.h declares (tests check they are all exported).
 ABI_SYMBOLS = ("rhg_target_radius", "rhg_band_boundaries", "rhg_workspace_bytes", "rhg_generate",
                "rhg_generate_with_radius", "rhg_generate_from_points", "rhg_sample_points",
-               "rhg_philox_words", "rhg_status_string", "rhg_version")
+               "rhg_philox_words", "rhg_status_string", "rhg_version", "rhg_last_cuda_error")
 
 
 class RhgError(RuntimeError):
@@ -102,13 +102,18 @@ def lib() -> ctypes.CDLL:
         L.rhg_status_string.argtypes = [ctypes.c_int]
         L.rhg_version.restype = ctypes.c_char_p
         L.rhg_version.argtypes = []
+        L.rhg_last_cuda_error.restype = ctypes.c_char_p
+        L.rhg_last_cuda_error.argtypes = []
         _lib = L
     return _lib
 
 
 def _check(status: int):
     if status != RHG_OK:
-        raise RhgError(status, lib().rhg_status_string(status).decode())
+        msg = lib().rhg_status_string(status).decode()
+        if status == RHG_ERR_CUDA:
+            msg += ": " + lib().rhg_last_cuda_error().decode()
+        raise RhgError(status, msg)
 
 
 def _torch():

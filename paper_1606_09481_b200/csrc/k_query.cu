@@ -34,11 +34,30 @@
 // whatever the range lengths.  The owner of a candidate is found with one
 // warp-wide OR of segment-start bits and a popcount (no search).  Hub vertices
 // take the chunked path at the end of this file.
+#include <cstdio>
 #include <type_traits>
 
 #include "rhg_internal.cuh"
 
 namespace rhg {
+
+// Debug builds (-DRHG_BOUNDS, scripts/): the first failed check is recorded in
+// DevScalars::dbg_line / dbg[] and printed by the host after the emit pass.
+#ifdef RHG_BOUNDS
+#define RHG_CHECK(cond)                                                      \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      if (atomicCAS(&A.sc->dbg_line, 0u, (unsigned)__LINE__) == 0u) {        \
+        A.sc->dbg[0] = blockIdx.x;                                           \
+        A.sc->dbg[1] = threadIdx.x;                                          \
+      }                                                                      \
+    }                                                                        \
+  } while (0)
+#else
+#define RHG_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 constexpr int QK_WARPS = 4;
 constexpr int QK_THREADS = QK_WARPS * 32;
@@ -344,6 +363,7 @@ constexpr int kCopyUnroll = 4;
 template <int FMT>
 __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long long o, uint32_t vid,
                                            uint32_t w) {
+  RHG_CHECK(o < A.out_cap);
 #if defined(RHG_EXP) && RHG_EXP == 1  // experiment: no output stores (loads kept alive)
   if (w == 0xFFFFFFFFu && o == 0) A.col[0] = w;
   return;

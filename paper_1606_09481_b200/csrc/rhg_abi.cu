@@ -201,6 +201,10 @@ cudaError_t& last_cuda_error() {
   static thread_local cudaError_t e = cudaSuccess;
   return e;
 }
+int& last_cuda_error_line() {
+  static thread_local int l = 0;
+  return l;
+}
 
 std::mutex g_pin_mu;
 DevScalars* g_pin = nullptr;  // page-locked readback slot
@@ -218,6 +222,7 @@ DevScalars* pinned_scalars() {
     cudaError_t e__ = (x);                     \
     if (e__ != cudaSuccess) {                  \
       last_cuda_error() = e__;                 \
+      last_cuda_error_line() = __LINE__;       \
       return RHG_ERR_CUDA;                     \
     }                                          \
   } while (0)
@@ -399,10 +404,24 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.offs = offs;
   qa.col = col_dev;
   qa.pairs = pairs_dev;
+  qa.out_cap = hs.total;
   // hub chunks replay their bits unless the hub bit buffer was too small (checked
   // on the device); light warps replay theirs unless they ran out of bit words.
   CK(launch_heavy(QM_EMIT_BITS, f, qa, ha, bc, st));
+#ifdef RHG_BOUNDS
+  CK(cudaStreamSynchronize(st));
+#endif
   CK(launch_query(QM_EMIT_BITS, f, qa, bc, st));  // warps whose bits overflowed re-test
+#ifdef RHG_BOUNDS
+  {
+    cudaError_t e = cudaStreamSynchronize(st);
+    DevScalars d;
+    cudaMemcpy(&d, sc, sizeof(d), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "RHG_BOUNDS: sync %s, check line %u block %llu thread %llu\n",
+            cudaGetErrorString(e), d.dbg_line, d.dbg[0], d.dbg[1]);
+    CK(e);
+  }
+#endif
   launches += 2;
   tm.mark();  // 6
   if (host) {
@@ -518,5 +537,12 @@ RHG_EXPORT const char* rhg_status_string(rhg_status s) {
 }
 
 RHG_EXPORT const char* rhg_version(void) { return RHG_VERSION; }
+
+RHG_EXPORT const char* rhg_last_cuda_error(void) {
+  static thread_local char buf[160];
+  snprintf(buf, sizeof(buf), "%s (rhg_abi.cu:%d)", cudaGetErrorString(last_cuda_error()),
+           last_cuda_error_line());
+  return buf;
+}
 
 }  // extern "C"

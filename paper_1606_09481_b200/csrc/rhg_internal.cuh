@@ -95,6 +95,8 @@ struct DevScalars {
   unsigned long long bit_words;    // candidate-bit words allocated by the count pass
   unsigned int domain_error;       // a point outside the disk
   unsigned int bit_overflow;       // bit buffer too small -> emit re-tests
+  unsigned int dbg_line;           // RHG_BOUNDS builds: first failed check (line, values)
+  unsigned long long dbg[3];
 };
 
 // One point in the query SoA, 32 B: theta, sinh r, e^{r/2}, e^{-r/2}.
@@ -115,6 +117,7 @@ struct QueryArgs {
   const uint64_t* __restrict__ offs;  // emit pass: output offset per vertex id
   uint32_t* col;                      // CSR output
   uint32_t* pairs;                    // undirected output
+  unsigned long long out_cap;         // elements col / pairs hold (debug bounds checks)
   uint32_t* bits;                     // light test bits: kLightBitRows x 32 words per light warp
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
