@@ -171,12 +171,12 @@ __device__ __forceinline__ bool certified_edge(double qth, double q4s, double qa
 
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));  // ftz: denormal ratios -> 0 (still a superset / subset)
   return y;
 }
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
-  asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 

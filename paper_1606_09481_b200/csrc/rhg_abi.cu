@@ -114,7 +114,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, sid2, dir, deg, offs,
-      scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
+      scan_tmp, heavy_scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
   size_t h_pstart, h_plen, h_poff, h_np, h_vtot, h_vtot_off, h_cc,
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
   size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
@@ -166,6 +166,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
     if ((uint64_t)kQuerySectors * kMaxBands > m) m = (uint64_t)kQuerySectors * kMaxBands;
     if (L.chunk_cap > m) m = L.chunk_cap;
     L.scan_tmp = take(scan_tmp_bytes(m));
+    L.heavy_scan_tmp = take(scan_tmp_bytes(m));
   }
   L.h_pstart = take(4 * L.nslots_cap);
   L.h_plen = take(4 * L.nslots_cap);
@@ -226,6 +227,24 @@ DevScalars* pinned_scalars() {
       return RHG_ERR_CUDA;                     \
     }                                          \
   } while (0)
+
+// Side stream for the hub path: the hub count / emit kernels run next to the light
+// kernels (they touch disjoint vertices and rows), forked from and joined back to
+// the caller's stream with events, so the caller still sees one stream.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+  SideStream() {
+    ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+SideStream& side_stream() {
+  static thread_local SideStream ss;
+  return ss;
+}
 
 struct Timer {
   bool on = false;
@@ -383,13 +402,20 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   ha.vcap = Lw.vcap;
   ha.chunk_cap = Lw.chunk_cap;
   ha.chunk_min = kChunkMin;
-  CK(launch_heavy_plan(f, qa, ha, bc, ws + Lw.scan_tmp, st, &launches));
-  CK(launch_heavy(QM_COUNT, f, qa, ha, bc, st));
+  // hub path on the side stream, light vertices on the caller's stream
+  SideStream& ss = side_stream();
+  if (!ss.ok) return RHG_ERR_CUDA;
+  CK(cudaEventRecord(ss.fork, st));
+  CK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  CK(launch_heavy_plan(f, qa, ha, bc, ws + Lw.heavy_scan_tmp, ss.s, &launches));
+  CK(launch_heavy(QM_COUNT, f, qa, ha, bc, ss.s));
   ++launches;
   CK(exclusive_scan_u32_u64_dev(ha.chunk_cap, &hmeta->nchunks, ha.chunk_hits, ha.chunk_pos,
-                                ws + Lw.scan_tmp, &hmeta->hits, st, &launches));
+                                ws + Lw.heavy_scan_tmp, &hmeta->hits, ss.s, &launches));
+  CK(cudaEventRecord(ss.join, ss.s));
   CK(launch_query(QM_COUNT, f, qa, bc, st));
   ++launches;
+  CK(cudaStreamWaitEvent(st, ss.join, 0));
   tm.mark();  // 4
   uint64_t* offs = (f == RHG_CSR) ? row_ptr_dev : offs_ws;
   CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
@@ -407,11 +433,15 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.out_cap = hs.total;
   // hub chunks replay their bits unless the hub bit buffer was too small (checked
   // on the device); light warps replay theirs unless they ran out of bit words.
-  CK(launch_heavy(QM_EMIT_BITS, f, qa, ha, bc, st));
+  CK(cudaEventRecord(ss.fork, st));
+  CK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
+  CK(launch_heavy(QM_EMIT_BITS, f, qa, ha, bc, ss.s));
+  CK(cudaEventRecord(ss.join, ss.s));
 #ifdef RHG_BOUNDS
-  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamSynchronize(ss.s));
 #endif
   CK(launch_query(QM_EMIT_BITS, f, qa, bc, st));  // warps whose bits overflowed re-test
+  CK(cudaStreamWaitEvent(st, ss.join, 0));
 #ifdef RHG_BOUNDS
   {
     cudaError_t e = cudaStreamSynchronize(st);
