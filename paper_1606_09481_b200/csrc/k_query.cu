@@ -169,6 +169,19 @@ __device__ __forceinline__ bool certified_edge(double qth, double q4s, double qa
   return act && (S4 <= T4);
 }
 
+// Same test when every candidate of the warp is known to have |dphi| < 2^-4 (and no
+// seam crossing): the short polynomial, which certified_edge also picks for such
+// pairs, so the decision is the same bit for bit from either endpoint.
+__device__ __forceinline__ bool certified_edge_short(double qth, double q4s, double qa, double qb,
+                                                     double2 w0, double2 w1, double T4, bool act) {
+  const double d = __dsub_rn(qth, w0.x);
+  const double sn = __dmul_rn(d, poly_short(__dmul_rn(d, d)));
+  const double Bv = __dmul_rn(sn, sn);
+  const double h = __dsub_rn(__dmul_rn(qa, w1.y), __dmul_rn(qb, w1.x));
+  const double C = __dmul_rn(__dmul_rn(q4s, w0.y), Bv);
+  return act && (__fma_rn(h, h, C) <= T4);
+}
+
 __device__ __forceinline__ float sqrt_approx(float x) {
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));  // ftz: denormal ratios -> 0 (still a superset / subset)
@@ -189,6 +202,7 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 template <typename I>
 struct SlabWin {
   I a, b, h0, h1, cs, ce;
+  int32_t dq;  // light kernel: outer half-width in quanta incl. bucket rounding (2^30 if full)
 };
 
 // num = T4 - 4 sinh^2((r_v - c_j)/2), num1 = the same at c_{j+1} (num1 of slab j
@@ -313,6 +327,7 @@ __device__ __forceinline__ void win32(const SlabC& S, int32_t q, double num, dou
   ls += sft; re += sft; cs += sft; ce += sft;
   if (!cert) ce = cs;
   // non-full: test [ls, re) minus [cs, ce); full: test [ce, cs + nj) (or all of it)
+  w.dq = full ? (1 << 30) : d_o + (1 << sh);
   w.cs = cert ? cs : 0;
   w.ce = cert ? ce : 0;
   if (full) {
@@ -544,6 +559,7 @@ __global__ void __launch_bounds__(QK_THREADS)
     const bool on = valid && (!outward || j >= (int)qband);
     SlabWin<I> w;
     w.a = w.b = w.h0 = w.h1 = w.cs = w.ce = 0;
+    w.dq = 0;
     if (on) {
       const double h0 = __fma_rn(q.a, S.B0, -__dmul_rn(q.b, S.A0));
       const double h1 = __fma_rn(q.a, S.B1, -__dmul_rn(q.b, S.A1));
@@ -554,9 +570,17 @@ __global__ void __launch_bounds__(QK_THREADS)
         SlabWin<int32_t> w32;
         win32(S, (int32_t)qq, num0, num1, qinv4s, bc.T4min, A.dir, w32);
         w.a = w32.a; w.b = w32.b; w.h0 = w32.h0; w.h1 = w32.h1; w.cs = w32.cs; w.ce = w32.ce;
+        w.dq = w32.dq;
       }
     }
+    // every candidate of the warp within |dphi| < 2^-4 (300000 quanta < 2^27 2^-4 / 2pi)
+    // and no window reaching across theta = 0 (so no seam pair): the short-polynomial
+    // test applies
+    const int32_t q32 = (int32_t)(qkey & kQMask);
+    const bool small = __all_sync(
+        FULL, !on || (!WIDE && w.dq < 300000 && q32 >= w.dq && q32 + w.dq < (int32_t)(1u << kQBits)));
     const bool own = on && (j == (int)qband);
+    const bool anyown = __any_sync(FULL, own);
     I e1 = 0, wx = 0;
     if (own) {
       const I kv = (I)(k - bstart);
@@ -626,16 +650,13 @@ __global__ void __launch_bounds__(QK_THREADS)
       bitpos = bp1;
       continue;
     }
-    for (uint32_t i = 0; i < mt; ++i) {
-      const bool act = i < nt;
-      const uint32_t p = pa + i + (i >= thr ? hl : 0u);
-      bool hit;
-      if (MODE == QM_EMIT_BITS && !retest) {
-        if ((bitpos & 31u) == 0) word = wbits[(bitpos >> 5) * 32u];
-        hit = act && ((word >> (bitpos & 31u)) & 1u);
-      } else {
-        const bool ex = (p - x1) < xw || (p - x1 - nj) < xw;
-        const bool tst = act && !ex;
+    // count, or emit with re-tests: every candidate is tested
+    auto test_loop = [&](auto short_poly) {
+      for (uint32_t i = 0; i < mt; ++i) {
+        const bool act = i < nt;
+        const uint32_t p = pa + i + (i >= thr ? hl : 0u);
+        bool tst = act;
+        if (anyown) tst = tst && !((p - x1) < xw || (p - x1 - nj) < xw);
         uint32_t r[8];
         const PointRec* wp = A.pts + (tst ? p : 0u);
         asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -644,23 +665,30 @@ __global__ void __launch_bounds__(QK_THREADS)
                      : "l"(wp));
         const double2 w0 = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
         const double2 w1 = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
-        hit = certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, tst);
-      }
-      if (MODE == QM_COUNT) {
-        deg += hit;
-        if (act) {  // the word of a group is stored at the group's end and at slab ends
-          word |= (uint32_t)hit << (bitpos & 31u);
-          const bool full = (bitpos & 31u) == 31u;
-          if (full || i + 1 == nt) {
-            if ((bitpos >> 5) < kLightBitRows) wbits[(bitpos >> 5) * 32u] = word;
+        const bool hit = decltype(short_poly)::value
+                             ? certified_edge_short(q.theta, q4s, q.a, q.b, w0, w1, T4, tst)
+                             : certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, tst);
+
+        if (MODE == QM_COUNT) {
+          deg += hit;
+          word |= (uint32_t)hit << (bitpos & 31u);  // hit is false for idle lanes
+          bitpos += act;
+          if (act && (bitpos & 31u) == 0) {  // a 32-test group completed
+            if ((bitpos >> 5) <= kLightBitRows) wbits[((bitpos >> 5) - 1) * 32u] = word;
             else over = true;
+            word = 0;
           }
-          if (full) word = 0;
+        } else if (hit) {
+          rw.put(A, qid, ld_keep(A.sid2 + p, keep));
         }
-      } else if (hit) {
-        rw.put(A, qid, ld_keep(A.sid2 + p, keep));
       }
-      if (act) ++bitpos;
+    };
+    if (small) test_loop(std::true_type{});
+    else test_loop(std::false_type{});
+    if (MODE != QM_COUNT) bitpos += nt;
+    if (MODE == QM_COUNT && nt > 0 && (bitpos & 31u)) {  // partial group: stored now, completed later
+      if ((bitpos >> 5) < kLightBitRows) wbits[(bitpos >> 5) * 32u] = word;
+      else over = true;
     }
   }
   if (MODE == QM_COUNT) {
