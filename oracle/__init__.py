@@ -81,6 +81,15 @@ def lib():
         L.orc_row_ties.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double, ctypes.c_uint32,
                                    _u32p, _u8p, ctypes.c_uint64]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_radius_from_C.restype = ctypes.c_double
+        L.orc_radius_from_C.argtypes = [ctypes.c_double] * 2
+        L.orc_movement_init.argtypes = [ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_double] * 4 + \
+            [_f64p, _f64p]
+        L.orc_rotate.restype = ctypes.c_double
+        L.orc_rotate.argtypes = [ctypes.c_double] * 2
+        L.orc_radial_step.argtypes = [ctypes.c_double] * 4 + [_f64p, _f64p]
+        L.orc_move_points.argtypes = [ctypes.c_uint64, _f64p, _f64p, _f64p, _f64p, ctypes.c_double,
+                                      ctypes.c_double]
         _lib = L
     return _lib
 
@@ -253,6 +262,43 @@ def row_ties(theta, r, R, v):
                            _p(e, _u8p), cap)
     c = min(c, cap)
     return w[:c].copy(), e[:c].astype(bool)
+
+
+# ---------------------------------------------------------------- f2 / f1
+def radius_from_C(n: float, C: float) -> float:
+    """R = 2 ln n + C."""
+    return lib().orc_radius_from_C(float(n), float(C))
+
+
+def movement_init(n: int, seed: int, phi_range=(-1.0, 1.0), r_range=(-10.0, 1.0)):
+    """Per-vertex step values (Appendix B ranges)."""
+    tp = np.zeros(n, dtype=np.float64)
+    tr = np.zeros(n, dtype=np.float64)
+    lib().orc_movement_init(n, seed, phi_range[0], phi_range[1], r_range[0], r_range[1],
+                            _p(tp, _f64p), _p(tr, _f64p))
+    return tp, tr
+
+
+def rotate(phi: float, tau_phi: float) -> float:
+    return lib().orc_rotate(phi, tau_phi)
+
+
+def radial_step(r: float, tau_r: float, R: float, alpha_: float):
+    ro = ctypes.c_double()
+    to = ctypes.c_double()
+    lib().orc_radial_step(r, tau_r, R, alpha_, ctypes.byref(ro), ctypes.byref(to))
+    return ro.value, to.value
+
+
+def move_points(theta, r, tau_phi, tau_r, R: float, alpha_: float):
+    """One movement step of every vertex (copies; tau_r returned with flipped signs)."""
+    th = np.array(theta, dtype=np.float64)
+    rr = np.array(r, dtype=np.float64)
+    tp = np.ascontiguousarray(tau_phi, dtype=np.float64)
+    tr = np.array(tau_r, dtype=np.float64)
+    lib().orc_move_points(len(th), _p(th, _f64p), _p(rr, _f64p), _p(tp, _f64p), _p(tr, _f64p),
+                          R, alpha_)
+    return th, rr, tr
 
 
 def num_threads() -> int:

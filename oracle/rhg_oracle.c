@@ -563,6 +563,78 @@ ORC_API int64_t orc_row_ties(uint64_t n, const double *theta, const double *r, d
   return (int64_t)c;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Radius parametrisation: "accept the commonly used      */
+/* parameter C, with R = 2 ln n + C".                                        */
+/* ------------------------------------------------------------------------ */
+ORC_API double orc_radius_from_C(double n, double C) { return 2.0 * log(n) + C; }
+
+/* ------------------------------------------------------------------------ */
+/* Dynamic model (Sec. 3.3).                              */
+/* Step values tau_phi, tau_r per vertex; Appendix B draws    */
+/* them uniformly from (-1, 1) and (-10, 1).  Reading     */
+/* D1: they come from Philox(key = seed, ctr = (i_lo, i_hi, 1,   */
+/* 0)), u1 -> tau_phi, u2 -> tau_r, mapped affinely onto [lo, hi).            */
+/* ------------------------------------------------------------------------ */
+ORC_API void orc_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi, double r_lo,
+                               double r_hi, double *tau_phi, double *tau_r) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; ++i) {
+    const uint32_t ctr[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 1u, 0u};
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    orc_philox4x32_10(ctr, key, w);
+    double u1, u2;
+    orc_uniforms(w, &u1, &u2);
+    tau_phi[i] = phi_lo + (phi_hi - phi_lo) * u1;
+    tau_r[i] = r_lo + (r_hi - r_lo) * u2;
+  }
+}
+
+/* Rotation step: rotated(phi, r, tau_phi) = (phi + tau_phi) mod 2pi,
+ * for |tau_phi| < 2pi: one add, then one wrap by fl(2pi); the result is kept in
+ * [0, fl(2pi)) (Reading Z10). */
+ORC_API double orc_rotate(double phi, double tau_phi) {
+  double s = phi + tau_phi;
+  if (s >= TWO_PI_HI) s -= TWO_PI_HI;
+  else if (s < 0.0) s += TWO_PI_HI;
+  if (s >= TWO_PI_HI || s < 0.0) s = 0.0;  /* rounding at the seam */
+  return s;
+}
+
+/* Radial step, Algorithm 2: x = sinh(r alpha), y = x + tau_r,
+ * z = asinh(y)/alpha.  Reflection: "if the new node position would
+ * be outside the boundary (r > R) or below the origin (r < 0), the movement is
+ * reflected and tau_r set to -tau_r".  Reading D2: reflect in the
+ * transformed coordinate y at 0 and at S = sinh(alpha R), once per crossing, and
+ * flip tau_r once per reflection. */
+ORC_API void orc_radial_step(double r, double tau_r, double R, double alpha, double *r_out,
+                             double *tau_out) {
+  const double S = sinh(alpha * R);
+  double y = sinh(r * alpha) + tau_r;
+  double t = tau_r;
+  for (int it = 0; it < 64 && (y < 0.0 || y > S); ++it) {
+    if (y < 0.0) y = -y;
+    else y = 2.0 * S - y;
+    t = -t;
+  }
+  if (y < 0.0) y = 0.0;
+  if (y > S) y = S;
+  double z = asinh(y) / alpha;
+  *r_out = z > R ? R : z;
+  *tau_out = t;
+}
+
+/* One movement step of every vertex, in place. */
+ORC_API void orc_move_points(uint64_t n, double *theta, double *r, const double *tau_phi,
+                             double *tau_r, double R, double alpha) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; ++i) {
+    theta[i] = orc_rotate(theta[i], tau_phi[i]);
+    orc_radial_step(r[i], tau_r[i], R, alpha, &r[i], &tau_r[i]);
+  }
+}
+
 ORC_API int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

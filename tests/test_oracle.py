@@ -395,3 +395,82 @@ def test_invariants_mean_degree_and_tail(orc):
         tail = k[k >= kmin]
         mle = 1 + len(tail) / np.sum(np.log(tail / (kmin - 0.5)))
         assert band[0] <= mle <= band[1]
+
+
+# ------------------------------------------------------------------ next rows (f1, f2)
+def test_radius_from_C_closed_form(orc):
+    """R = 2 ln n + C: n = e^5, C = 0 gives R = 10; C shifts R."""
+    assert orc.radius_from_C(np.exp(5.0), 0.0) == pytest.approx(10.0, abs=1e-12)
+    assert orc.radius_from_C(np.exp(5.0), -1.5) == pytest.approx(8.5, abs=1e-12)
+
+
+def test_rotate_spec_example_and_range(orc):
+    """rotated(phi, tau) = (phi + tau) mod 2pi."""
+    assert orc.rotate(1.0, 0.0) == 1.0
+    assert orc.rotate(6.0, 1.0) == pytest.approx(7.0 - 2 * np.pi, abs=1e-15)   # 0.7168
+    assert orc.rotate(0.5, -1.0) == pytest.approx(2 * np.pi - 0.5, abs=1e-15)
+    rng = np.random.default_rng(4)
+    for phi, tau in zip(rng.uniform(0, 2 * np.pi, 2000), rng.uniform(-1, 1, 2000)):
+        x = orc.rotate(phi, tau)
+        assert 0.0 <= x < 2 * np.pi
+        assert np.cos(x) == pytest.approx(np.cos(phi + tau), abs=1e-12)
+
+
+def test_radial_step_algorithm2(orc):
+    """Alg. 2: SPEC.md:356 example, identity for tau = 0, and the
+    inverse move (r, tau) then (r', -tau) without reflection."""
+    r1, t1 = orc.radial_step(1.0, 1.0, 10.0, 1.0)
+    assert r1 == pytest.approx(1.5194, abs=1e-4) and t1 == 1.0
+    assert r1 == pytest.approx(np.arcsinh(np.sinh(1.0) + 1.0), abs=1e-15)
+    rng = np.random.default_rng(5)
+    for a in (0.6, 1.0, 1.7):
+        R = 20.0
+        for r, tau in zip(rng.uniform(5, 19, 200), rng.uniform(-1, 1, 200)):  # no reflection
+            assert orc.radial_step(r, 0.0, R, a) == (pytest.approx(r, rel=4e-15), 0.0)
+            r2, t2 = orc.radial_step(r, tau, R, a)
+            r3, t3 = orc.radial_step(r2, -t2, R, a)
+            assert t2 == tau and r3 == pytest.approx(r, rel=1e-12)
+
+
+def test_radial_step_reflection(orc):
+    """Reflection: the result stays in [0, R]; tau flips iff the
+    transformed coordinate left [0, sinh(alpha R)] (Reading D2, folded back)."""
+    R, a = 10.0, 1.0
+    S = np.sinh(a * R)
+    r, t = orc.radial_step(0.5, -3.0, R, a)        # y = sinh(0.5) - 3 < 0 -> folded at 0
+    assert t == 3.0 and r == pytest.approx(np.arcsinh(3.0 - np.sinh(0.5)), rel=1e-14)
+    r, t = orc.radial_step(R - 1e-3, 1e3, R, a)    # y > S -> folded at S
+    assert t == -1e3 and r == pytest.approx(np.arcsinh(2 * S - np.sinh(R - 1e-3) - 1e3), rel=1e-12)
+    rng = np.random.default_rng(6)
+    for r0, tau in zip(rng.uniform(0, R, 3000), rng.uniform(-50, 50, 3000)):
+        r1, t1 = orc.radial_step(r0, tau, R, a)
+        assert 0.0 <= r1 <= R
+        y = np.sinh(a * r0) + tau
+        assert (t1 == -tau) == (y < 0 or y > S)
+
+
+def test_movement_init_ranges(orc):
+    """Step values uniform on the Appendix B ranges, Philox
+    counter (i, 1) so they are independent of the point sample (counter (i, 0))."""
+    tp, tr = orc.movement_init(50_000, 3)
+    assert tp.min() >= -1 and tp.max() < 1 and tr.min() >= -10 and tr.max() < 1
+    assert stats.kstest((tp + 1) / 2, "uniform").pvalue > 1e-3
+    assert stats.kstest((tr + 10) / 11, "uniform").pvalue > 1e-3
+    w = orc.philox4x32_10([7, 0, 1, 0], [3, 0])
+    u1 = (int(w[1]) << 32 | int(w[0])) >> 11
+    assert tp[7] == pytest.approx(-1 + 2 * u1 * 2.0**-53, abs=0)
+
+
+def test_theorem1_distribution_preserved(orc):
+    """Theorem 1: 100 movement steps of 10^4 vertices keep the
+    radial marginal at F(r) and the angular one uniform (KS at 0.01)."""
+    n, a = 10_000, 1.0
+    R = 2 * np.log(n) + 2
+    th, r = orc.sample_points(n, a, R, 7)
+    tp, tr = orc.movement_init(n, 9)
+    F = lambda x: (np.cosh(a * x) - 1) / (np.cosh(a * R) - 1)
+    crit = 1.628 / np.sqrt(n)
+    for _ in range(100):
+        th, r, tr = orc.move_points(th, r, tp, tr, R, a)
+        assert stats.kstest(r, F).statistic < crit
+    assert stats.kstest(th / (2 * np.pi), "uniform").statistic < crit
