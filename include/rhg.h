@@ -137,6 +137,27 @@ rhg_status rhg_generate(uint64_t n, double kbar, double gamma, uint64_t seed,
 rhg_status rhg_generate_with_radius(uint64_t n, double R, double alpha, uint64_t seed,
                                     const rhg_output *out, rhg_stream stream);
 
+/* Same with the disk radius from the parameter C: R = 2 ln n + C ("accept the
+   commonly used parameter C"); alpha > 1/2. */
+rhg_status rhg_generate_with_C(uint64_t n, double C, double alpha, uint64_t seed,
+                               const rhg_output *out, rhg_stream stream);
+
+/* Dynamic model (Sec. 3.3).
+   rhg_movement_init: per-vertex step values drawn uniformly from
+   [phi_lo, phi_hi) and [r_lo, r_hi) (Appendix B uses (-1, 1) and (-10, 1),
+   PAPER.md:526-529) by Philox(key = seed, counter = (i, 1)) -- independent of the
+   point sample (counter (i, 0)).  Device arrays tau_phi[n], tau_r[n]; |phi_*| < 2pi.
+   rhg_move_points: one movement step of every vertex, in place on device arrays:
+   theta <- (theta + tau_phi) mod 2pi; r <- Algorithm 2
+   (x = sinh(alpha r), y = x + tau_r, r = asinh(y)/alpha) with the
+   reflection of PAPER.md:254 applied in y at 0 and sinh(alpha R): tau_r changes
+   sign once per reflection.  The graph of the moved points is rebuilt with
+   rhg_generate_from_points (the exact edge set of the new positions). */
+rhg_status rhg_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi, double r_lo,
+                             double r_hi, double *tau_phi, double *tau_r, rhg_stream stream);
+rhg_status rhg_move_points(uint64_t n, double *theta, double *r, const double *tau_phi,
+                           double *tau_r, double R, double alpha, rhg_stream stream);
+
 /* Edges of a given point set (Alg. 1 lines 9-21): theta[n] in [0, 2pi),
    r[n] in [0, R], fp64, device pointers (host if out->host_buffers).  Ids are
    the input indices.  Out-of-domain points -> RHG_ERR_DOMAIN. */

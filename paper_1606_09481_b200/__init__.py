@@ -30,7 +30,8 @@ FORMATS = {"csr": RHG_CSR, "edges": RHG_EDGES_UNDIRECTED, "pairs": RHG_EDGES_UND
 # Symbols include/rhg.h declares (tests check they are all exported).
 ABI_SYMBOLS = ("rhg_target_radius", "rhg_band_boundaries", "rhg_workspace_bytes", "rhg_generate",
                "rhg_generate_with_radius", "rhg_generate_from_points", "rhg_sample_points",
-               "rhg_philox_words", "rhg_status_string", "rhg_version", "rhg_last_cuda_error")
+               "rhg_philox_words", "rhg_status_string", "rhg_version", "rhg_last_cuda_error",
+               "rhg_generate_with_C", "rhg_movement_init", "rhg_move_points")
 
 
 class RhgError(RuntimeError):
@@ -102,6 +103,12 @@ def lib() -> ctypes.CDLL:
         L.rhg_status_string.argtypes = [ctypes.c_int]
         L.rhg_version.restype = ctypes.c_char_p
         L.rhg_version.argtypes = []
+        L.rhg_generate_with_C.restype = st
+        L.rhg_generate_with_C.argtypes = [u64, f64, f64, u64, ctypes.POINTER(Output), vp]
+        L.rhg_movement_init.restype = st
+        L.rhg_movement_init.argtypes = [u64, u64, f64, f64, f64, f64, vp, vp, vp]
+        L.rhg_move_points.restype = st
+        L.rhg_move_points.argtypes = [u64, vp, vp, vp, vp, f64, f64, vp]
         L.rhg_last_cuda_error.restype = ctypes.c_char_p
         L.rhg_last_cuda_error.argtypes = []
         _lib = L
@@ -270,6 +277,37 @@ def generate_with_radius(n: int, R: float, alpha: float, seed: int, fmt: str = "
                 kbar_hint, device=device, capacity=capacity, options=options, timing=timing,
                 workspace=workspace, stream=stream, host_buffers=host_buffers,
                 want_points=return_points, sample=True)
+
+
+def generate_with_C(n: int, C: float, alpha: float, seed: int, fmt: str = "csr", *,
+                    device="cuda", capacity=None, options=None, timing=False, workspace=None,
+                    stream=None, host_buffers=False, return_points=False, kbar_hint=None) -> Graph:
+    """R = 2 ln n + C."""
+    L = lib()
+    return _run(lambda o, s: L.rhg_generate_with_C(n, C, alpha, seed, o, s), n, fmt, kbar_hint,
+                device=device, capacity=capacity, options=options, timing=timing,
+                workspace=workspace, stream=stream, host_buffers=host_buffers,
+                want_points=return_points, sample=True)
+
+
+def movement_init(n: int, seed: int, phi_range=(-1.0, 1.0), r_range=(-10.0, 1.0), device="cuda",
+                  stream=None):
+    """Per-vertex step values of the dynamic model (Appendix B ranges)."""
+    torch = _torch()
+    tp = torch.empty(n, dtype=torch.float64, device=device)
+    tr = torch.empty(n, dtype=torch.float64, device=device)
+    _check(lib().rhg_movement_init(n, seed, phi_range[0], phi_range[1], r_range[0], r_range[1],
+                                   tp.data_ptr(), tr.data_ptr(), _stream_handle(stream)))
+    return tp, tr
+
+
+def move_points(theta, r, tau_phi, tau_r, R: float, alpha: float, stream=None):
+    """One movement step in place (rotation + Alg. 2 with reflection).
+    All four are contiguous float64 CUDA tensors; tau_r changes sign on reflection."""
+    for t in (theta, r, tau_phi, tau_r):
+        assert t.is_cuda and t.dtype == _torch().float64 and t.is_contiguous()
+    _check(lib().rhg_move_points(theta.numel(), theta.data_ptr(), r.data_ptr(), tau_phi.data_ptr(),
+                                 tau_r.data_ptr(), R, alpha, _stream_handle(stream)))
 
 
 def generate_from_points(theta, r, R: float, fmt: str = "csr", *, capacity=None, options=None,

@@ -528,6 +528,36 @@ RHG_EXPORT rhg_status rhg_generate(uint64_t n, double kbar, double gamma, uint64
   return rhg_generate_with_radius(n, R, (gamma - 1.0) / 2.0, seed, out, stream);
 }
 
+RHG_EXPORT rhg_status rhg_generate_with_C(uint64_t n, double C, double alpha, uint64_t seed,
+                                          const rhg_output* out, rhg_stream stream) {
+  if (!std::isfinite(C) || n < 2) return RHG_ERR_INVALID;
+  const double R = 2.0 * std::log((double)n) + C;
+  if (!(R >= 0.0)) return RHG_ERR_INVALID;
+  return rhg_generate_with_radius(n, R, alpha, seed, out, stream);
+}
+
+RHG_EXPORT rhg_status rhg_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi,
+                                        double r_lo, double r_hi, double* tau_phi, double* tau_r,
+                                        rhg_stream stream) {
+  if (!tau_phi || !tau_r || !std::isfinite(phi_lo) || !std::isfinite(phi_hi) ||
+      !std::isfinite(r_lo) || !std::isfinite(r_hi) || !(phi_hi >= phi_lo) || !(r_hi >= r_lo) ||
+      !(phi_lo > -6.283185307179586) || !(phi_hi < 6.283185307179586))
+    return RHG_ERR_INVALID;
+  if (n == 0) return RHG_OK;
+  CK(launch_movement_init(n, seed, phi_lo, phi_hi, r_lo, r_hi, tau_phi, tau_r, (cudaStream_t)stream));
+  return RHG_OK;
+}
+
+RHG_EXPORT rhg_status rhg_move_points(uint64_t n, double* theta, double* r, const double* tau_phi,
+                                      double* tau_r, double R, double alpha, rhg_stream stream) {
+  if (!theta || !r || !tau_phi || !tau_r || !(alpha > 0.5) || !std::isfinite(alpha) ||
+      !(R > 0.0) || !std::isfinite(std::sinh(alpha * R)))
+    return RHG_ERR_INVALID;
+  if (n == 0) return RHG_OK;
+  CK(launch_move(n, theta, r, tau_phi, tau_r, R, alpha, (cudaStream_t)stream));
+  return RHG_OK;
+}
+
 RHG_EXPORT rhg_status rhg_generate_from_points(uint64_t n, const double* theta, const double* r, double R,
                                     const rhg_output* out, rhg_stream stream) {
   return run(n, false, 0.0, 0, theta, r, R, out, (cudaStream_t)stream);

@@ -212,4 +212,11 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
 cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                          const BandConst& bc, cudaStream_t st);
 
+// Dynamic model (k_dynamic.cu)
+cudaError_t launch_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi,
+                                 double r_lo, double r_hi, double* tau_phi, double* tau_r,
+                                 cudaStream_t st);
+cudaError_t launch_move(uint64_t n, double* theta, double* r, const double* tau_phi, double* tau_r,
+                        double R, double alpha, cudaStream_t st);
+
 }  // namespace rhg

@@ -23,7 +23,7 @@ def rhg():
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "rhg.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rhg_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(rhg_[A-Za-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_header_symbols(rhg):

@@ -312,3 +312,65 @@ def test_full_size_pairs_sampled_degrees(rhg, orc):
     _sampled_rows_check(row, orc, th_o, r_o, R, q)
     mean = 2 * g.num_edges / n
     assert abs(mean - kbar) / kbar < 0.03
+
+
+# --------------------------------------------------------------------------- next rows f1, f2
+def test_generate_with_C(rhg, orc):
+    """R = 2 ln n + C: the GPU edge set equals the oracle's brute force
+    on the same points with the oracle's own R."""
+    n, C, a, seed = 8_000, -2.0, 0.9, 21
+    R = orc.radius_from_C(n, C)
+    g = rhg.generate_with_C(n, C, a, seed, "csr", return_points=True)
+    assert g.R == R
+    th, r = orc.sample_points(n, a, R, seed)
+    assert np.array_equal(g.theta.cpu().numpy(), th)
+    es = orc.brute_force(th, r, R)
+    compare_sets(csr_checked_pairs(g), es)
+
+
+def test_movement_init_bit_exact(rhg, orc):
+    tp, tr = rhg.movement_init(100_003, 77, (-1.0, 1.0), (-10.0, 1.0))
+    tpo, tro = orc.movement_init(100_003, 77, (-1.0, 1.0), (-10.0, 1.0))
+    assert np.array_equal(tp.cpu().numpy(), tpo) and np.array_equal(tr.cpu().numpy(), tro)
+
+
+def test_move_points_matches_oracle_and_rebuild(rhg, orc):
+    """One movement step on the GPU vs the oracle's step (rotation bit-exact; the
+    radial step to a few ulp: device vs glibc sinh/asinh; reflections identical),
+    then the graph of the moved points vs the oracle's brute force on them."""
+    n, kbar, gamma, seed = 20_000, 10, 2.6, 31
+    th, r, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    tp, tr = orc.movement_init(n, 5, (-1.0, 1.0), (-10.0, 1.0))
+    tr[:50] = -np.sinh(a * r[:50]) * 3.0   # force reflections at the origin
+    tr[50:100] = np.sinh(a * R) * 0.5       # and at the rim
+    g_th, g_r = torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda()
+    g_tp, g_tr = torch.from_numpy(tp).cuda(), torch.from_numpy(tr.copy()).cuda()
+    rhg.move_points(g_th, g_r, g_tp, g_tr, R, a)
+    th1, r1, tr1 = orc.move_points(th, r, tp, tr, R, a)
+    assert np.array_equal(g_th.cpu().numpy(), th1)
+    gr = g_r.cpu().numpy()
+    assert np.all(np.abs(gr - r1) <= 8 * np.spacing(np.maximum(r1, 1e-300)) + 1e-300)
+    assert np.array_equal(np.sign(g_tr.cpu().numpy()), np.sign(tr1))
+    assert np.all(g_tr.cpu().numpy()[:100] == -tr[:100])
+    assert gr.min() >= 0 and gr.max() <= R
+    es = orc.brute_force(g_th.cpu().numpy(), gr, R)
+    for fmt in ("csr", "pairs"):
+        g = rhg.generate_from_points(g_th, g_r, R, fmt)
+        compare_sets(csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g), es)
+
+
+def test_theorem1_on_gpu(rhg, orc):
+    """Theorem 1 for the GPU movement: 100 steps of 10^4 vertices
+    keep the radial marginal at F(r) and the angles uniform (KS at 0.01)."""
+    from scipy import stats
+    n, a = 10_000, 1.0
+    R = 2 * np.log(n) + 2
+    th, r = rhg.sample_points(n, a, R, 7)
+    tp, tr = rhg.movement_init(n, 9)
+    F = lambda x: (np.cosh(a * x) - 1) / (np.cosh(a * R) - 1)
+    crit = 1.628 / np.sqrt(n)
+    for _ in range(100):
+        rhg.move_points(th, r, tp, tr, R, a)
+    torch.cuda.synchronize()
+    assert stats.kstest(r.cpu().numpy(), F).statistic < crit
+    assert stats.kstest(th.cpu().numpy() / (2 * np.pi), "uniform").statistic < crit
