@@ -341,7 +341,7 @@ def test_move_points_matches_oracle_and_rebuild(rhg, orc):
     n, kbar, gamma, seed = 20_000, 10, 2.6, 31
     th, r, R, a = oracle_points(orc, n, kbar, gamma, seed)
     tp, tr = orc.movement_init(n, 5, (-1.0, 1.0), (-10.0, 1.0))
-    tr[:50] = -np.sinh(a * r[:50]) * 3.0   # force reflections at the origin
+    tr[:50] = -np.sinh(a * r[:50]) * 1.5   # force one reflection at the origin
     tr[50:100] = 1.25 * np.sinh(a * R) - np.sinh(a * r[50:100])  # and once at the rim
     g_th, g_r = torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda()
     g_tp, g_tr = torch.from_numpy(tp).cuda(), torch.from_numpy(tr.copy()).cuda()
