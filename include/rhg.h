@@ -158,6 +158,33 @@ rhg_status rhg_movement_init(uint64_t n, uint64_t seed, double phi_lo, double ph
 rhg_status rhg_move_points(uint64_t n, double *theta, double *r, const double *tau_phi,
                            double *tau_r, double R, double alpha, rhg_stream stream);
 
+/* On-device validation statistics. */
+#define RHG_STATS_BINS 40
+typedef struct {
+  uint64_t num_edges;      /* undirected edges                                           */
+  uint64_t max_degree;
+  double mean_degree;      /* 2m / n                                                     */
+  uint64_t tail_count;     /* vertices with degree >= k_min                              */
+  double tail_exponent;    /* discrete MLE 1 + N / sum ln(k / (k_min - 1/2)) over k >= k_min
+                              (compare with gamma = 2 alpha + 1); 0 if no tail */
+  uint64_t near_ties;      /* emitted edges with |cosh d - cosh R| <= 1e-12 cosh R
+                              (the north star's excused window); ~0 if no points given      */
+  uint64_t degree_hist[RHG_STATS_BINS]; /* [0]: degree 0; [b]: degree in [2^(b-1), 2^b)   */
+} rhg_stats;
+
+/* Scratch for rhg_graph_stats (device, caller-owned). */
+size_t rhg_stats_workspace_bytes(uint64_t n);
+
+/* Statistics of a graph produced by this library, computed on the device:
+   format RHG_CSR: row_ptr[n+1], col (device); RHG_EDGES_UNDIRECTED: pairs[2m]
+   (device), m undirected edges.  theta/r (device, vertex-id order, optional):
+   the points, for the near-tie count.  Synchronises `stream` once. */
+rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint64_t *row_ptr,
+                           const uint32_t *col, const uint32_t *pairs, uint64_t m,
+                           const double *theta, const double *r, double R, double k_min,
+                           void *workspace, size_t workspace_bytes, rhg_stats *out,
+                           rhg_stream stream);
+
 /* Edges of a given point set (Alg. 1 lines 9-21): theta[n] in [0, 2pi),
    r[n] in [0, R], fp64, device pointers (host if out->host_buffers).  Ids are
    the input indices.  Out-of-domain points -> RHG_ERR_DOMAIN. */

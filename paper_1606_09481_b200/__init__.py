@@ -31,7 +31,9 @@ FORMATS = {"csr": RHG_CSR, "edges": RHG_EDGES_UNDIRECTED, "pairs": RHG_EDGES_UND
 ABI_SYMBOLS = ("rhg_target_radius", "rhg_band_boundaries", "rhg_workspace_bytes", "rhg_generate",
                "rhg_generate_with_radius", "rhg_generate_from_points", "rhg_sample_points",
                "rhg_philox_words", "rhg_status_string", "rhg_version", "rhg_last_cuda_error",
-               "rhg_generate_with_C", "rhg_movement_init", "rhg_move_points")
+               "rhg_generate_with_C", "rhg_movement_init", "rhg_move_points",
+               "rhg_stats_workspace_bytes", "rhg_graph_stats")
+STATS_BINS = 40
 
 
 class RhgError(RuntimeError):
@@ -56,6 +58,18 @@ class Timing(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("num_edges", ctypes.c_uint64), ("max_degree", ctypes.c_uint64),
+                ("mean_degree", ctypes.c_double), ("tail_count", ctypes.c_uint64),
+                ("tail_exponent", ctypes.c_double), ("near_ties", ctypes.c_uint64),
+                ("degree_hist", ctypes.c_uint64 * 40)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "degree_hist"}
+        d["degree_hist"] = list(self.degree_hist)
+        return d
 
 
 class Output(ctypes.Structure):
@@ -109,6 +123,11 @@ def lib() -> ctypes.CDLL:
         L.rhg_movement_init.argtypes = [u64, u64, f64, f64, f64, f64, vp, vp, vp]
         L.rhg_move_points.restype = st
         L.rhg_move_points.argtypes = [u64, vp, vp, vp, vp, f64, f64, vp]
+        L.rhg_stats_workspace_bytes.restype = ctypes.c_size_t
+        L.rhg_stats_workspace_bytes.argtypes = [u64]
+        L.rhg_graph_stats.restype = st
+        L.rhg_graph_stats.argtypes = [u64, ctypes.c_int, vp, vp, vp, u64, vp, vp, f64, f64, vp,
+                                      ctypes.c_size_t, ctypes.POINTER(Stats), vp]
         L.rhg_last_cuda_error.restype = ctypes.c_char_p
         L.rhg_last_cuda_error.argtypes = []
         _lib = L
@@ -308,6 +327,28 @@ def move_points(theta, r, tau_phi, tau_r, R: float, alpha: float, stream=None):
         assert t.is_cuda and t.dtype == _torch().float64 and t.is_contiguous()
     _check(lib().rhg_move_points(theta.numel(), theta.data_ptr(), r.data_ptr(), tau_phi.data_ptr(),
                                  tau_r.data_ptr(), R, alpha, _stream_handle(stream)))
+
+
+def graph_stats(g: "Graph", theta=None, r=None, k_min: float = 10.0, stream=None) -> dict:
+    """On-device validation statistics (degree histogram, mean/max degree, tail MLE,
+    near-tie edges) of a graph from this library.  theta/r: the
+    points (CUDA, vertex-id order) for the near-tie count."""
+    torch = _torch()
+    L = lib()
+    dev = g.row_ptr.device if g.format == "csr" else g.pairs.device
+    ws = torch.empty(int(L.rhg_stats_workspace_bytes(g.n)), dtype=torch.uint8, device=dev)
+    out = Stats()
+    if g.format == "csr":
+        args = (RHG_CSR, g.row_ptr.data_ptr(), g.col.data_ptr() if g.col.numel() else None, None, 0)
+    else:
+        args = (RHG_EDGES_UNDIRECTED, None, None, g.pairs.data_ptr() if g.num_edges else None,
+                g.num_edges)
+    _check(L.rhg_graph_stats(g.n, *args, _ptr(theta), _ptr(r), g.R, k_min, ws.data_ptr(),
+                             ws.numel(), ctypes.byref(out), _stream_handle(stream)))
+    d = out.as_dict()
+    if theta is None:
+        d["near_ties"] = None
+    return d
 
 
 def generate_from_points(theta, r, R: float, fmt: str = "csr", *, capacity=None, options=None,

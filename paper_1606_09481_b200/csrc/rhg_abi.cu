@@ -558,6 +558,24 @@ RHG_EXPORT rhg_status rhg_move_points(uint64_t n, double* theta, double* r, cons
   return RHG_OK;
 }
 
+RHG_EXPORT size_t rhg_stats_workspace_bytes(uint64_t n) { return stats_workspace_bytes(n); }
+
+RHG_EXPORT rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint64_t* row_ptr,
+                                      const uint32_t* col, const uint32_t* pairs, uint64_t m,
+                                      const double* theta, const double* r, double R, double k_min,
+                                      void* workspace, size_t workspace_bytes, rhg_stats* out,
+                                      rhg_stream stream) {
+  if (!out || n == 0 || n > (1ull << 31) || !workspace ||
+      workspace_bytes < stats_workspace_bytes(n) || !(k_min >= 1.0) || !std::isfinite(R))
+    return RHG_ERR_INVALID;
+  if (format == RHG_CSR && (!row_ptr || (!col && (theta || r)))) return RHG_ERR_INVALID;
+  if (format == RHG_EDGES_UNDIRECTED && !pairs && m) return RHG_ERR_INVALID;
+  if (format != RHG_CSR && format != RHG_EDGES_UNDIRECTED) return RHG_ERR_INVALID;
+  CK(launch_graph_stats((uint32_t)n, format, row_ptr, col, pairs, m, theta, r, R, k_min, workspace,
+                        out, (cudaStream_t)stream));
+  return RHG_OK;
+}
+
 RHG_EXPORT rhg_status rhg_generate_from_points(uint64_t n, const double* theta, const double* r, double R,
                                     const rhg_output* out, rhg_stream stream) {
   return run(n, false, 0.0, 0, theta, r, R, out, (cudaStream_t)stream);

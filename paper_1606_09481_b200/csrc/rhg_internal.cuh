@@ -2,6 +2,7 @@
 // orchestration).  Nothing here is shared with oracle/ (see DESIGN.md).
 #pragma once
 #include <cuda_runtime.h>
+#include <cmath>
 #include <stdint.h>
 
 #include "../../include/rhg.h"
@@ -211,6 +212,13 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
                               const BandConst& bc, void* scan_tmp, cudaStream_t st, int* launches);
 cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                          const BandConst& bc, cudaStream_t st);
+
+// Validation statistics (k_stats.cu)
+size_t stats_workspace_bytes(uint64_t n);
+cudaError_t launch_graph_stats(uint32_t n, int fmt, const uint64_t* row_ptr, const uint32_t* col,
+                               const uint32_t* pairs, uint64_t m, const double* theta,
+                               const double* r, double R, double kmin, void* ws,
+                               rhg_stats* host_out, cudaStream_t st);
 
 // Dynamic model (k_dynamic.cu)
 cudaError_t launch_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi,

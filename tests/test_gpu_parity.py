@@ -374,3 +374,56 @@ def test_theorem1_on_gpu(rhg, orc):
     torch.cuda.synchronize()
     assert stats.kstest(r.cpu().numpy(), F).statistic < crit
     assert stats.kstest(th.cpu().numpy() / (2 * np.pi), "uniform").statistic < crit
+
+
+# --------------------------------------------------------------------------- next row f4
+def test_graph_stats_match_host(rhg, orc):
+    """On-device statistics equal the same quantities computed on the host from the
+    oracle's edge set (degrees, histogram, mean/max, MLE formula of SPEC.md:427-435)."""
+    n, kbar, gamma, seed = 20_000, 12, 2.4, 41
+    th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    es = orc.brute_force(th, r, R)
+    deg = np.bincount(es.pairs.ravel().astype(np.int64), minlength=n)
+    kmin = 10.0
+    tail = deg[deg >= kmin].astype(np.float64)
+    mle = 1 + len(tail) / np.sum(np.log(tail / (kmin - 0.5)))
+    hist = np.zeros(40, dtype=np.int64)
+    for d in deg:
+        hist[0 if d == 0 else min(int(d).bit_length(), 39)] += 1
+    pt = torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda()
+    for fmt in ("csr", "pairs"):
+        g = rhg.generate_from_points(*pt, R, fmt)
+        st = rhg.graph_stats(g, *pt, k_min=kmin)
+        assert st["num_edges"] == es.m and st["max_degree"] == deg.max()
+        assert st["mean_degree"] == pytest.approx(2 * es.m / n, rel=1e-12)
+        assert st["tail_count"] == len(tail)
+        assert st["tail_exponent"] == pytest.approx(mle, rel=1e-9)
+        assert st["degree_hist"] == hist.tolist()
+        assert st["near_ties"] <= len(es.ties) + 2
+
+
+def test_graph_stats_powerlaw_synthetic(rhg):
+    """degrees drawn i.i.d. from a discrete power law with exponent 3
+    give a tail MLE of 3 +- 0.1 for 10^5 samples (a CSR with those row lengths)."""
+    rng = np.random.default_rng(8)
+    kmin, n = 10, 100_000
+    # inverse-transform sampling of P(k) ~ k^-3 on k >= kmin (continuous approx + floor)
+    u = rng.random(n)
+    k = np.floor((kmin - 0.5) * (1 - u) ** (-1 / 2.0) + 0.5).astype(np.int64)
+    row_ptr = torch.from_numpy(np.concatenate([[0], np.cumsum(k)])).cuda()
+    col = torch.zeros(int(k.sum()), dtype=torch.int32, device="cuda")
+    g = rhg.Graph(n=n, format="csr", R=10.0, num_edges=int(k.sum()), row_ptr=row_ptr, col=col)
+    st = rhg.graph_stats(g, k_min=float(kmin))
+    assert abs(st["tail_exponent"] - 3.0) < 0.1
+    assert st["near_ties"] is None
+
+
+def test_graph_stats_full_size_invariants(rhg):
+    """Config 3 at full size, no host copy of the graph: mean degree within 3 % of
+    kbar (Reading Z14), tail exponent near gamma (Z15), near-tie edges ~0."""
+    n, kbar, gamma, seed = CONFIGS[3]
+    g = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True)
+    st = rhg.graph_stats(g, g.theta, g.r, k_min=2 * kbar)
+    assert st["mean_degree"] == pytest.approx(kbar, rel=0.03)
+    assert 2.6 <= st["tail_exponent"] <= 3.4
+    assert st["near_ties"] <= 2
