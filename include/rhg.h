@@ -64,7 +64,16 @@ typedef struct {
   double band_ratio; /* p, geometric width ratio; 0 -> 0.9 */
   uint32_t heavy_threshold; /* candidates of one (vertex, slab) range above which the range is
                                split across warps; 0 -> library default */
-  int reserved[5];
+  /* Sharding: with shard_count = N > 1 the call emits only
+     the edges owned by shard shard_index: the rows (CSR) or the outward edges (list)
+     of 1/N of the light query order and 1/N of the hub vertices.  Every shard samples
+     and indexes the whole point set; rows of vertices owned by other shards are
+     empty, so the N outputs are disjoint and their union is the graph.  Output
+     (row contents included) is identical to the unsharded call's for owned vertices.
+     0 / 1 -> one shard. */
+  int shard_index;
+  int shard_count;
+  int reserved[3];
 } rhg_options;
 
 /* Per-phase device times (CUDA events on the caller's stream), filled when

@@ -44,7 +44,8 @@ class RhgError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("num_bands", ctypes.c_int), ("band_ratio", ctypes.c_double),
-                ("heavy_threshold", ctypes.c_uint32), ("reserved", ctypes.c_int * 5)]
+                ("heavy_threshold", ctypes.c_uint32), ("shard_index", ctypes.c_int),
+                ("shard_count", ctypes.c_int), ("reserved", ctypes.c_int * 3)]
 
 
 class Timing(ctypes.Structure):
@@ -181,9 +182,10 @@ def workspace_bytes(n: int, fmt: str = "csr", capacity: int = 0, host_buffers: b
 
 def _options(options) -> Options:
     if options is None:
-        return Options(0, 0.0, 0)
+        return Options(0, 0.0, 0, 0, 0)
     return Options(int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
-                   int(options.get("heavy_threshold", 0)))
+                   int(options.get("heavy_threshold", 0)), int(options.get("shard_index", 0)),
+                   int(options.get("shard_count", 0)))
 
 
 def version() -> str:
@@ -327,6 +329,44 @@ def move_points(theta, r, tau_phi, tau_r, R: float, alpha: float, stream=None):
         assert t.is_cuda and t.dtype == _torch().float64 and t.is_contiguous()
     _check(lib().rhg_move_points(theta.numel(), theta.data_ptr(), r.data_ptr(), tau_phi.data_ptr(),
                                  tau_r.data_ptr(), R, alpha, _stream_handle(stream)))
+
+
+def shard_offsets(counts) -> list:
+    """Exclusive prefix of the per-shard edge counts: where shard s's edges start in
+    the concatenation of all shards' outputs."""
+    out, acc = [], 0
+    for c in counts:
+        out.append(acc)
+        acc += int(c)
+    return out + [acc]
+
+
+def distributed_generate(n: int, kbar: float, gamma: float, seed: int, fmt: str = "csr", *,
+                         group=None, device=None, **kw):
+    """One graph sharded over the ranks of a torch.distributed group (one process per
+    GPU): every rank samples and indexes all points, generates the edges it owns
+    (shard = rank of world) and the ranks exchange one 8-byte edge count each
+    (all_gather) for the global offsets.  Returns (graph shard, offsets, total)."""
+    import torch.distributed as dist
+    torch = _torch()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    opts = dict(kw.pop("options", None) or {})
+    opts.update(shard_index=rank, shard_count=world)
+    g = generate(n, kbar, gamma, seed, fmt, device=device or "cuda", options=opts, **kw)
+    offsets, total = exchange_counts(g.num_edges, group=group)
+    return g, offsets, total
+
+
+def exchange_counts(num_edges: int, group=None):
+    """all_gather of one uint64 edge count per rank -> (offsets, total)."""
+    import torch.distributed as dist
+    torch = _torch()
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    mine = torch.tensor([num_edges], dtype=torch.int64, device=dev)
+    parts = [torch.zeros_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, mine, group=group)
+    offs = shard_offsets([int(p.item()) for p in parts])
+    return offs[:-1], offs[-1]
 
 
 def graph_stats(g: "Graph", theta=None, r=None, k_min: float = 10.0, stream=None) -> dict:

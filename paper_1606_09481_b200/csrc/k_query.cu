@@ -519,10 +519,14 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint32_t g = blockIdx.x * QK_WARPS + (threadIdx.x >> 5);  // light warp
+  const uint32_t g = blockIdx.x * QK_WARPS + (threadIdx.x >> 5);  // light warp (of this shard)
   const uint32_t nlight = A.n - A.lay->heavy_end;
-  if (g * 32u >= nlight) return;
-  const uint32_t idx = g * 32u + lane;
+  // shard: a contiguous range of the 32-vertex groups of the sector-major order
+  const uint32_t ngroups = (nlight + 31u) / 32u;
+  const uint32_t gbeg = (uint32_t)shard_begin(ngroups, bc.shard, bc.nshards);
+  const uint32_t gend = (uint32_t)shard_begin(ngroups, bc.shard + 1, bc.nshards);
+  if (gbeg + g >= gend) return;
+  const uint32_t idx = (gbeg + g) * 32u + lane;
   const bool valid = idx < nlight;
   const uint32_t k = valid ? __ldg(A.order + idx) : 0u;
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
@@ -740,12 +744,14 @@ __global__ void __launch_bounds__(HV_THREADS)
   const int L = bc.L;
   const uint32_t LS = kRangesPerSlab * (uint32_t)L;
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
+  const uint32_t hbeg = (uint32_t)shard_begin(he, bc.shard, bc.nshards);
+  const uint32_t hend = (uint32_t)shard_begin(he, bc.shard + 1, bc.nshards);
   for (uint32_t i = gw; i < he; i += TW) {
     const uint32_t qkey = A.skey[i];
     const uint32_t qband = qkey >> kBandShift;
     const PointRec q = A.pts[i + bs.start[qband]];
     const double qinv4s = 0.25 / q.s;
-    const int j = lane;
+    const int j = (i >= hbeg && i < hend) ? lane : 32;  // other shards' hubs: no pieces
     int64_t lo[6] = {0, 0, 0, 0, 0, 0}, ln[6] = {0, 0, 0, 0, 0, 0};
     uint32_t gbase = 0;
     if (j < L) {
@@ -981,7 +987,8 @@ cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
 
 cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const BandConst& bc,
                          cudaStream_t st) {
-  const uint32_t groups = (qa.n + 31) / 32;
+  // warps for this shard's groups (upper bound: hubs are excluded on the device)
+  const uint32_t groups = ((qa.n + 31) / 32 + bc.nshards - 1) / bc.nshards + 1;
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
   const bool wide = qa.n >= (1u << 30);  // a slab may hold >= 2^30 points: 64-bit positions

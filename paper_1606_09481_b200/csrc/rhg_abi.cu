@@ -106,6 +106,11 @@ rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandCon
   bc->T4min = bc->T4 * 0x1.0p-10;
   bc->heavy_threshold = (opt && opt->heavy_threshold) ? (double)opt->heavy_threshold : 1024.0;
   bc->heavy_cap = (uint32_t)heavy_cap_for(n);
+  const int ns = (opt && opt->shard_count > 1) ? opt->shard_count : 1;
+  const int si = (opt && ns > 1) ? opt->shard_index : 0;
+  if (si < 0 || si >= ns || ns > 4096) return RHG_ERR_INVALID;
+  bc->shard = (uint32_t)si;
+  bc->nshards = (uint32_t)ns;
   return RHG_OK;
 }
 
@@ -383,6 +388,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.warp_over = (uint32_t*)(ws + Lw.b_over);
   qa.deg = deg;
   qa.sc = sc;
+  if (bc.nshards > 1) CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of other shards stay empty
   HeavyArgs ha{};
   ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
   ha.plen = (uint32_t*)(ws + Lw.h_plen);

@@ -39,6 +39,7 @@ struct BandConst {
   double T4min;              // 2^-10 T4: certain windows need T4 - h^2 above this at both ends
   double heavy_threshold;    // expected candidates per vertex above which a slab's vertices are hubs
   uint32_t heavy_cap;        // at most this many hub vertices (workspace bound)
+  uint32_t shard, nshards;   // this call owns shard `shard` of `nshards` (1: everything)
 };
 
 // Device-computed band layout after the band histogram.
@@ -123,6 +124,11 @@ struct QueryArgs {
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
 };
+
+// Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.
+__host__ __device__ __forceinline__ uint64_t shard_begin(uint64_t T, uint32_t s, uint32_t N) {
+  return T * s / N;
+}
 
 // ---- K1 device code shared by the sampler and the generate-path gather ----
 // Philox4x32-10 (Salmon et al. 2011): counter (i_lo, i_hi, 0, 0), key = seed.

@@ -58,3 +58,30 @@ def test_reference_arm_other_ranks_exit_silently(capsys):
     finally:
         os.environ.pop("RANK")
     assert capsys.readouterr().out == ""
+
+
+def _exchange_worker(rank, world, port, q):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1606_09481_b200 as rhg
+    offs, total = rhg.exchange_counts([1000, 234][rank])
+    q.put((rank, offs, total))
+    dist.destroy_process_group()
+
+
+def test_shard_count_exchange_gloo_world2():
+    """The one collective of the sharded path: all_gather of one edge count per rank
+     -> global offsets, over gloo with world size 2."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict((r, (o, t)) for r, o, t in [q.get(timeout=120) for _ in ps])
+    for p in ps:
+        p.join(timeout=60)
+    assert res[0] == ([0, 1000], 1234) and res[1] == ([0, 1000], 1234)

@@ -427,3 +427,34 @@ def test_graph_stats_full_size_invariants(rhg):
     assert st["mean_degree"] == pytest.approx(kbar, rel=0.03)
     assert 2.6 <= st["tail_exponent"] <= 3.4
     assert st["near_ties"] <= 2
+
+
+# --------------------------------------------------------------------------- sharding (f3)
+@pytest.mark.parametrize("fmt,cfg", [("csr", 4), ("pairs", 4), ("csr", 2)])
+def test_shards_partition_the_graph(rhg, fmt, cfg):
+    """N shards of one graph: disjoint outputs whose union is the
+    unsharded graph; the rows of owned vertices are identical to the unsharded rows."""
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    full = rhg.generate(n, kbar, gamma, seed, fmt)
+    N = 3
+    parts = [rhg.generate(n, kbar, gamma, seed, fmt, options=dict(shard_index=s, shard_count=N))
+             for s in range(N)]
+    assert sum(p.num_edges for p in parts) == full.num_edges
+    if fmt == "csr":
+        rp = full.row_ptr.cpu().numpy()
+        col = full.col.cpu().numpy()
+        deg_sum = np.zeros(n, dtype=np.int64)
+        for p in parts:
+            prp = p.row_ptr.cpu().numpy()
+            pcol = p.col.cpu().numpy()
+            d = np.diff(prp)
+            deg_sum += d
+            own = np.nonzero(d)[0]
+            for v in own[:: max(1, len(own) // 500)]:
+                assert np.array_equal(pcol[prp[v]:prp[v + 1]], col[rp[v]:rp[v + 1]])
+        assert np.array_equal(deg_sum, np.diff(rp))
+    else:
+        a = np.sort(keys_of(full.pairs.cpu().numpy()))
+        b = np.sort(np.concatenate([keys_of(p.pairs.cpu().numpy()) for p in parts]))
+        assert np.array_equal(a, b)
+    assert rhg.shard_offsets([p.num_edges for p in parts])[-1] == full.num_edges
