@@ -73,7 +73,15 @@ typedef struct {
      0 / 1 -> one shard. */
   int shard_index;
   int shard_count;
-  int reserved[3];
+  /* Vertex ids.  0 (default): vertex i is the i-th sample (Philox counter i) or
+     the i-th input point.  1: ids in the order of Alg. 1 lines 9-12 (PAPER.md:
+     150-155): slab by slab (inner to outer), by angular key within a slab
+     (floor(theta 2^27 / 2pi), ties by sample index).  Same graph, relabelled;
+     rows are then written without gathering ids (faster emit).
+     rhg_output.perm_out, if set, receives perm[id] = sample / input index.
+     theta_out / r_out stay in sample order. */
+  int vertex_order;
+  int reserved[2];
 } rhg_options;
 
 /* Per-phase device times (CUDA events on the caller's stream), filled when
@@ -113,6 +121,8 @@ typedef struct {
   double *R_used;          /* HOST, optional: the disk radius used                             */
   const rhg_options *options; /* optional, NULL -> defaults                                    */
   rhg_timing *timing;      /* HOST, optional                                                  */
+  uint32_t *perm_out;      /* optional n-array, written when options->vertex_order = 1:
+                              perm_out[id] = sample / input index of vertex id            */
 } rhg_output;
 
 /* getTargetRadius: R such that Eq. 22 (zeta = 1) gives kbar,

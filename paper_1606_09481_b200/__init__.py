@@ -45,7 +45,8 @@ class RhgError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("num_bands", ctypes.c_int), ("band_ratio", ctypes.c_double),
                 ("heavy_threshold", ctypes.c_uint32), ("shard_index", ctypes.c_int),
-                ("shard_count", ctypes.c_int), ("reserved", ctypes.c_int * 3)]
+                ("shard_count", ctypes.c_int), ("vertex_order", ctypes.c_int),
+                ("reserved", ctypes.c_int * 2)]
 
 
 class Timing(ctypes.Structure):
@@ -80,7 +81,8 @@ class Output(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t), ("theta_out", ctypes.c_void_p),
                 ("r_out", ctypes.c_void_p), ("num_edges", ctypes.POINTER(ctypes.c_uint64)),
                 ("R_used", ctypes.POINTER(ctypes.c_double)),
-                ("options", ctypes.POINTER(Options)), ("timing", ctypes.POINTER(Timing))]
+                ("options", ctypes.POINTER(Options)), ("timing", ctypes.POINTER(Timing)),
+                ("perm_out", ctypes.c_void_p)]
 
 
 _lib = None
@@ -185,7 +187,7 @@ def _options(options) -> Options:
         return Options(0, 0.0, 0, 0, 0)
     return Options(int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
                    int(options.get("heavy_threshold", 0)), int(options.get("shard_index", 0)),
-                   int(options.get("shard_count", 0)))
+                   int(options.get("shard_count", 0)), int(options.get("vertex_order", 0)))
 
 
 def version() -> str:
@@ -205,6 +207,7 @@ class Graph:
     theta: object = None
     r: object = None
     timing: dict = field(default_factory=dict)
+    perm: object = None            # vertex_order = 1: torch int32 [n], perm[id] = sample index
 
     @property
     def num_undirected(self) -> int:
@@ -254,13 +257,17 @@ def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspac
             pairs = torch.empty((max(cap, 1), 2), dtype=torch.int32, **kw) if f != RHG_CSR else None
             theta = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
             r = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
+        perm = None
+        if opts.vertex_order == 1:
+            kw = dict(device="cpu", pin_memory=True) if host_buffers else dict(device=device)
+            perm = torch.empty(n, dtype=torch.int32, **kw)
         ne = ctypes.c_uint64()
         Ru = ctypes.c_double()
         tm = Timing()
         out = Output(f, int(host_buffers), _ptr(row_ptr), _ptr(col), _ptr(pairs), cap,
                      wbuf.data_ptr(), wbuf.numel(), _ptr(theta), _ptr(r), ctypes.pointer(ne),
                      ctypes.pointer(Ru), ctypes.pointer(opts),
-                     ctypes.pointer(tm) if timing else None)
+                     ctypes.pointer(tm) if timing else None, _ptr(perm))
         st = call(ctypes.byref(out), _stream_handle(stream))
         if st == RHG_ERR_CAPACITY and capacity is None and attempt == 0:
             cap = int(ne.value)
@@ -268,7 +275,7 @@ def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspac
         _check(st)
         m = int(ne.value)
         g = Graph(n=n, format=fmt, R=Ru.value, num_edges=m, theta=theta, r=r,
-                  timing=tm.as_dict() if timing else {})
+                  timing=tm.as_dict() if timing else {}, perm=perm)
         if f == RHG_CSR:
             g.row_ptr, g.col = row_ptr, col[:m]
         else:

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256)
     k_gather(uint32_t n, const double* __restrict__ theta, const double* __restrict__ r,
              const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
              const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
-             uint32_t* __restrict__ sid2) {
+             uint32_t* __restrict__ sid2, int seq_ids) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t i = sidx[k];
     const double rr = r[i];
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256)
     p.s = sinh(rr);
     p.a = exp(0.5 * rr);
     p.b = exp(-0.5 * rr);
-    put_doubled(k, skey[k], lay, p, i, pts, sid2);
+    put_doubled(k, skey[k], lay, p, seq_ids ? k : i, pts, sid2);
   }
 }
 
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256)
     k_gather_philox(uint32_t n, uint64_t seed, double two_over_alpha, double half_span, double R,
                     const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
                     const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
-                    uint32_t* __restrict__ sid2) {
+                    uint32_t* __restrict__ sid2, int seq_ids) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t i = sidx[k];
     double th, rr;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256)
     p.s = sinh(rr);
     p.a = exp(0.5 * rr);
     p.b = exp(-0.5 * rr);
-    put_doubled(k, skey[k], lay, p, i, pts, sid2);
+    put_doubled(k, skey[k], lay, p, seq_ids ? k : i, pts, sid2);
   }
 }
 
@@ -133,15 +133,16 @@ __global__ void __launch_bounds__(256)
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
                                int L, PointRec* pts, uint32_t* sid2, uint32_t* dir,
-                               const PhiloxPoints* gen, cudaStream_t st, int* launches) {
+                               const PhiloxPoints* gen, int seq_ids, cudaStream_t st,
+                               int* launches) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
   if (gen)
     k_gather_philox<<<blocks, 256, 0, st>>>(n, gen->seed, gen->two_over_alpha, gen->half_span,
-                                            gen->R, skey, sidx, lay, pts, sid2);
+                                            gen->R, skey, sidx, lay, pts, sid2, seq_ids);
   else
-    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, skey, sidx, lay, pts, sid2);
+    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, skey, sidx, lay, pts, sid2, seq_ids);
   k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
   if (launches) *launches += 2;
   return cudaGetLastError();

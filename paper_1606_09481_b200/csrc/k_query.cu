@@ -469,6 +469,89 @@ struct RowWriter {
   }
 };
 
+// Row writer for sequential vertex ids (rhg_options.vertex_order = 1: the id of a
+// vertex is its position in the (slab, angle) order, so the ids of a certain piece
+// are consecutive integers and the id of a tested candidate is its position).
+// The lane assembles its current 32-byte output sector in eight registers: a run
+// of consecutive ids or a single id is merged in with per-slot selects (no
+// shared memory, no loads), and a completed sector leaves as one STG.256.  The
+// sectors holding the row's first and last slots are written slot by slot.
+// Pairs (u, v) = (the query vertex, the partner): the partner's id is larger.
+template <int FMT>
+struct SecWriter {
+  static constexpr uint32_t EPS = FMT == RHG_CSR ? 8u : 4u;  // elements per sector
+  uint32_t r[8];
+  uint32_t f;                      // filled elements of the current sector
+  unsigned long long sec, start;   // current sector, first element of the row
+  __device__ __forceinline__ void init(unsigned long long pos, uint32_t vid) {
+    sec = pos / EPS;
+    f = (uint32_t)(pos % EPS);
+    start = pos;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) r[x] = vid;  // pairs: even words stay = vid
+  }
+  __device__ __forceinline__ void store_slots(const QueryArgs& A, uint32_t lo, uint32_t hi) {
+#pragma unroll
+    for (uint32_t x = 0; x < EPS; ++x) {
+      if (x >= lo && x < hi) {
+        if (FMT == RHG_CSR) A.col[sec * EPS + x] = r[x];
+        else reinterpret_cast<uint2*>(A.pairs)[sec * EPS + x] = make_uint2(r[2 * x], r[2 * x + 1]);
+      }
+    }
+  }
+  __device__ __forceinline__ void flush(const QueryArgs& A) {
+    const unsigned long long s0 = sec * EPS;
+    RHG_CHECK(s0 + EPS <= A.out_cap);
+    if (s0 >= start) {
+      uint32_t* dst = FMT == RHG_CSR ? A.col + s0 : A.pairs + 2 * s0;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]),
+                   "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                   : "memory");
+    } else {
+      store_slots(A, (uint32_t)(start - s0), EPS);
+    }
+    ++sec;
+    f = 0;
+  }
+  // ids v0, v0 + 1, ..., v0 + len - 1 (all lanes call; len may be 0)
+  __device__ __forceinline__ void run(const QueryArgs& A, uint32_t v0, uint32_t len) {
+    while (__any_sync(FULL, len != 0)) {
+      const uint32_t t = min(len, EPS - f);
+      const uint32_t base = v0 - f;
+#pragma unroll
+      for (uint32_t x = 0; x < EPS; ++x) {
+        const bool in = (x - f) < t;
+        if (FMT == RHG_CSR) r[x] = in ? base + x : r[x];
+        else r[2 * x + 1] = in ? base + x : r[2 * x + 1];
+      }
+      f += t;
+      v0 += t;
+      len -= t;
+      if (f == EPS) flush(A);
+    }
+  }
+  __device__ __forceinline__ void put(const QueryArgs& A, uint32_t v) {
+#pragma unroll
+    for (uint32_t x = 0; x < EPS; ++x) {
+      if (FMT == RHG_CSR) r[x] = x == f ? v : r[x];
+      else r[2 * x + 1] = x == f ? v : r[2 * x + 1];
+    }
+    if (++f == EPS) flush(A);
+  }
+  __device__ __forceinline__ void finish(const QueryArgs& A) {
+    if (f) {
+      const unsigned long long s0 = sec * EPS;
+      store_slots(A, s0 >= start ? 0u : (uint32_t)(start - s0), f);
+    }
+  }
+};
+
+// id of doubled position p of a slab starting at s with nj points (sequential ids)
+__device__ __forceinline__ uint32_t seq_id(uint32_t p, uint32_t s, uint32_t nj) {
+  const uint32_t x = p - 2u * s;
+  return s + (x >= nj ? x - nj : x);
+}
+
 __device__ __forceinline__ uint4 ld4_keep(const uint32_t* ptr, uint64_t pol) {
   uint4 v;
   asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
@@ -493,13 +576,17 @@ __device__ __forceinline__ double inv4s_of(double s) {
 #ifndef RHG_QK_MINB_EMIT
 #define RHG_QK_MINB_EMIT 9
 #endif
-template <int MODE, int FMT, bool WIDE>
-__global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COUNT : RHG_QK_MINB_EMIT)
+#ifndef RHG_QK_MINB_SEQ
+#define RHG_QK_MINB_SEQ 7  // 72 registers: the eight sector registers of SecWriter
+#endif
+template <int MODE, int FMT, bool WIDE, bool SEQ>
+__global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COUNT
+                                              : (SEQ ? RHG_QK_MINB_SEQ : RHG_QK_MINB_EMIT))
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
   __shared__ BandSm bs;
   __shared__ SlabC scs[kMaxBands];
-  __shared__ uint32_t stage_all[MODE == QM_COUNT ? 1 : QK_THREADS * kStageStride];
+  __shared__ uint32_t stage_all[(MODE == QM_COUNT || SEQ) ? 1 : QK_THREADS * kStageStride];
   load_band_sm(bs, A.lay, bc.L);
   if (threadIdx.x < (unsigned)bc.L) {
     const int j = threadIdx.x;
@@ -536,7 +623,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   uint32_t qkey = 0, qid = 0;
   if (valid) {
     qkey = __ldg(A.skey + k);
-    qid = __ldg(A.sid + k);
+    if (MODE != QM_COUNT) qid = SEQ ? k : __ldg(A.sid + k);
   }
   const uint32_t qband = qkey >> kBandShift;
   const I qq = (I)(qkey & kQMask);
@@ -547,9 +634,15 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   const double q4s = 4.0 * q.s;
 
   RowWriter<FMT> rw;
+  SecWriter<FMT> sw;
   if (MODE != QM_COUNT) {
-    rw.stage = stage_all + threadIdx.x * kStageStride;
-    rw.pos = rw.start = valid ? A.offs[qid] : 0ull;
+    const unsigned long long pos0 = valid ? A.offs[qid] : 0ull;
+    if (SEQ) {
+      sw.init(pos0, qid);
+    } else {
+      rw.stage = stage_all + threadIdx.x * kStageStride;
+      rw.pos = rw.start = pos0;
+    }
   }
   uint32_t deg = 0;           // count pass
   uint32_t bitpos = 0, word = 0;
@@ -604,6 +697,15 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     if (MODE == QM_COUNT) {
       deg += ct;
       certain += ct;
+    } else if (SEQ) {
+      // ---- certain edges: consecutive ids, two pieces, each wrapping at most once ----
+      const uint32_t rel0 = (uint32_t)clo0 >= nj ? (uint32_t)clo0 - nj : (uint32_t)clo0;
+      const uint32_t rel1 = (uint32_t)clo1 >= nj ? (uint32_t)clo1 - nj : (uint32_t)clo1;
+      const uint32_t a0 = min((uint32_t)cln0, nj - rel0), a1 = min((uint32_t)cln1, nj - rel1);
+      sw.run(A, bstart + rel0, a0);
+      sw.run(A, bstart, (uint32_t)cln0 - a0);
+      sw.run(A, bstart + rel1, a1);
+      sw.run(A, bstart, (uint32_t)cln1 - a1);
     } else {
       // ---- certain edges: copy the ids into my row, 4 aligned ids per load ----
       const uint32_t c0 = gbase + (uint32_t)clo0, c1 = gbase + (uint32_t)clo1;
@@ -653,7 +755,8 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
             const uint32_t i = wb + (uint32_t)(__ffs(m) - 1) - bp0;
             m &= m - 1u;
             const uint32_t p = pa + i + (i >= thr ? hl : 0u);
-            rw.put(A, qid, ld_keep(A.sid2 + p, keep));
+            if (SEQ) sw.put(A, seq_id(p, bstart, nj));
+            else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
           }
         }
       }
@@ -688,6 +791,8 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
             else over = true;
             word = 0;
           }
+        } else if (SEQ) {
+          if (hit) sw.put(A, seq_id(p, bstart, nj));
         } else if (hit) {
           rw.put(A, qid, ld_keep(A.sid2 + p, keep));
         }
@@ -702,7 +807,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     }
   }
   if (MODE == QM_COUNT) {
-    if (valid) A.deg[qid] = deg;
+    if (valid) A.deg[A.labels ? k : __ldg(A.sid + k)] = deg;
     const bool anyover = __any_sync(FULL, over);
     if (lane == 0) {
       A.warp_over[g] = anyover ? 1u : 0u;
@@ -715,7 +820,8 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
       atomicAdd(&A.sc->certain, certain);
     }
   } else if (valid) {
-    rw.finish(A);
+    if (SEQ) sw.finish(A);
+    else rw.finish(A);
   }
 }
 
@@ -800,7 +906,7 @@ __global__ void __launch_bounds__(HV_THREADS)
       H.np[i] = ci;
       H.vtot[i] = ca;
     }
-    if (lane == 0) A.deg[A.sid[i]] = 0u;
+    if (lane == 0) A.deg[A.labels ? i : A.sid[i]] = 0u;
   }
 }
 
@@ -872,7 +978,7 @@ __global__ void __launch_bounds__(HV_THREADS, 4)
     const uint32_t vt = H.vtot[i];
     const uint32_t hi = (uint32_t)min((unsigned long long)vt, (unsigned long long)lo + CH);
     const uint32_t np = H.np[i];
-    const uint32_t qid = A.sid[i];
+    const uint32_t qid = A.labels ? i : A.sid[i];
     unsigned long long base = 0;
     if (MODE != QM_COUNT) base = A.offs[qid] + (H.chunk_pos[c] - H.chunk_pos[c0]);
     const uint32_t qband = A.skey[i] >> kBandShift;
@@ -992,20 +1098,29 @@ cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
   const bool wide = qa.n >= (1u << 30);  // a slab may hold >= 2^30 points: 64-bit positions
-#define RHG_LQ(M, F)                                                                   \
+#define RHG_LQ(M, F, S)                                                                \
   do {                                                                                 \
-    if (wide) k_query<M, F, true><<<blocks, QK_THREADS, 0, st>>>(qa, bc);              \
-    else k_query<M, F, false><<<blocks, QK_THREADS, 0, st>>>(qa, bc);                  \
+    if (wide) k_query<M, F, true, S><<<blocks, QK_THREADS, 0, st>>>(qa, bc);           \
+    else k_query<M, F, false, S><<<blocks, QK_THREADS, 0, st>>>(qa, bc);               \
   } while (0)
-  if (mode == QM_COUNT) {
-    if (fmt == RHG_CSR) RHG_LQ(QM_COUNT, RHG_CSR);
-    else RHG_LQ(QM_COUNT, RHG_EDGES_UNDIRECTED);
+  const bool seq = qa.labels != 0;
+  if (mode == QM_COUNT) {  // the count pass does not write ids
+    if (fmt == RHG_CSR) RHG_LQ(QM_COUNT, RHG_CSR, false);
+    else RHG_LQ(QM_COUNT, RHG_EDGES_UNDIRECTED, false);
   } else if (mode == QM_EMIT) {
-    if (fmt == RHG_CSR) RHG_LQ(QM_EMIT, RHG_CSR);
-    else RHG_LQ(QM_EMIT, RHG_EDGES_UNDIRECTED);
+    if (fmt == RHG_CSR) {
+      if (seq) RHG_LQ(QM_EMIT, RHG_CSR, true); else RHG_LQ(QM_EMIT, RHG_CSR, false);
+    } else {
+      if (seq) RHG_LQ(QM_EMIT, RHG_EDGES_UNDIRECTED, true);
+      else RHG_LQ(QM_EMIT, RHG_EDGES_UNDIRECTED, false);
+    }
   } else {
-    if (fmt == RHG_CSR) RHG_LQ(QM_EMIT_BITS, RHG_CSR);
-    else RHG_LQ(QM_EMIT_BITS, RHG_EDGES_UNDIRECTED);
+    if (fmt == RHG_CSR) {
+      if (seq) RHG_LQ(QM_EMIT_BITS, RHG_CSR, true); else RHG_LQ(QM_EMIT_BITS, RHG_CSR, false);
+    } else {
+      if (seq) RHG_LQ(QM_EMIT_BITS, RHG_EDGES_UNDIRECTED, true);
+      else RHG_LQ(QM_EMIT_BITS, RHG_EDGES_UNDIRECTED, false);
+    }
   }
 #undef RHG_LQ
   return cudaGetLastError();

@@ -293,6 +293,8 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   // device outputs are written in whole 32-byte sectors (k_query): 32-byte alignment
   if (!host && (((uintptr_t)out->col | (uintptr_t)out->pairs) & 31)) return RHG_ERR_INVALID;
   if (!sample && (!theta_in || !r_in)) return RHG_ERR_INVALID;
+  const int order = out->options ? out->options->vertex_order : 0;
+  if (order != 0 && order != 1) return RHG_ERR_INVALID;
   BandConst bc;
   rhg_status s = make_band_const(n, R, out->options, &bc);
   if (s != RHG_OK) return s;
@@ -369,14 +371,18 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
                 &launches));
   tm.mark();  // 2
   CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, sid2, dir,
-                        sample ? &gen : nullptr, st, &launches));
+                        sample ? &gen : nullptr, order, st, &launches));
   CK(launch_query_order(keys_a, lay, bc.L, (uint32_t*)(ws + Lw.q_cell_lo),
                         (uint32_t*)(ws + Lw.q_cell_cnt), (uint64_t*)(ws + Lw.q_cell_off),
                         (uint32_t*)(ws + Lw.q_order), ws + Lw.scan_tmp, st, &launches));
   tm.mark();  // 3
 
+  if (order == 1 && out->perm_out)  // id (sorted position) -> sample / input index
+    CK(cudaMemcpyAsync(out->perm_out, vals_a, 4 * n,
+                       host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
   QueryArgs qa{};
   qa.n = (uint32_t)n;
+  qa.labels = (uint32_t)order;
   qa.pts = pts;
   qa.skey = keys_a;
   qa.sid = vals_a;

@@ -123,6 +123,7 @@ struct QueryArgs {
   uint32_t* bits;                     // light test bits: kLightBitRows x 32 words per light warp
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
+  uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
 };
 
 // Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.
@@ -193,7 +194,8 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
 cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const uint32_t* skey, const uint32_t* sidx, const BandLayout* lay,
                                int L, PointRec* pts, uint32_t* sid2, uint32_t* dir,
-                               const PhiloxPoints* gen, cudaStream_t st, int* launches);
+                               const PhiloxPoints* gen, int seq_ids, cudaStream_t st,
+                               int* launches);
 // Sector-major order of the light queries (k_index.cu); cell arrays hold
 // kQuerySectors * L entries (cell_off: + 1).
 cudaError_t launch_query_order(const uint32_t* skey, const BandLayout* lay, int L,

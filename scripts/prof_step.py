@@ -19,13 +19,15 @@ ap.add_argument("--fmt", default=None)
 ap.add_argument("--heavy", type=int, default=0)
 ap.add_argument("--bands", type=int, default=0)
 ap.add_argument("--ratio", type=float, default=0.0)
+ap.add_argument("--order", type=int, default=0)
 a = ap.parse_args()
 n, kbar, gamma, seed, fmt = CFG[a.cfg]
 fmt = a.fmt or fmt
 ws = rhg.Workspace("cuda")
-opts = {"heavy_threshold": a.heavy, "num_bands": a.bands, "band_ratio": a.ratio}
+opts = {"heavy_threshold": a.heavy, "num_bands": a.bands, "band_ratio": a.ratio,
+        "vertex_order": a.order}
 for i in range(a.reps):
     g = rhg.generate(n, kbar, gamma, seed, fmt, workspace=ws, timing=True, options=opts)
     torch.cuda.synchronize()
     t = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in g.timing.items()}
-    print(json.dumps({"cfg": a.cfg, "fmt": fmt, "L": a.bands, "p": a.ratio, "m": g.num_edges, **t}))
+    print(json.dumps({"cfg": a.cfg, "order": a.order, "fmt": fmt, "L": a.bands, "p": a.ratio, "m": g.num_edges, **t}))

@@ -458,3 +458,59 @@ def test_shards_partition_the_graph(rhg, fmt, cfg):
         b = np.sort(np.concatenate([keys_of(p.pairs.cpu().numpy()) for p in parts]))
         assert np.array_equal(a, b)
     assert rhg.shard_offsets([p.num_edges for p in parts])[-1] == full.num_edges
+
+
+# --------------------------------------------------------------------------- vertex order
+def relabel_keys(keys, perm):
+    """Canonical (u < v) keys of id-space edges mapped through perm (id -> sample)."""
+    u = perm[(keys >> np.uint64(32)).astype(np.int64)].astype(np.uint64)
+    v = perm[(keys & np.uint64(0xFFFFFFFF)).astype(np.int64)].astype(np.uint64)
+    lo, hi = np.minimum(u, v), np.maximum(u, v)
+    return np.sort((lo << np.uint64(32)) | hi)
+
+
+@pytest.mark.parametrize("cfg,fmt", [(1, "csr"), (1, "pairs"), (2, "csr"), (2, "pairs"),
+                                     (4, "csr"), (4, "pairs")])
+def test_sorted_vertex_order_matches_oracle(rhg, orc, cfg, fmt):
+    """vertex_order = 1: ids follow (slab, angle); mapped back through perm the edge
+    set is the oracle's, and the order is the one rhg.h documents."""
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    es = orc.brute_force(th, r, R) if n <= 20_000 else orc.sweep(th, r, R)
+    g = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R, fmt,
+                                 options=dict(vertex_order=1))
+    perm = g.perm.cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(np.sort(perm), np.arange(n)), "perm is not a permutation"
+    gk = csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g)
+    compare_sets(relabel_keys(gk, perm), es)
+    # ids run slab by slab, by angle within a slab (keys of 2^27 angular quanta)
+    c = rhg.band_boundaries(n, R)
+    band = np.clip(np.searchsorted(c, r[perm], side="right") - 1, 0, len(c) - 2)
+    assert np.all(np.diff(band) >= 0)
+    same = np.diff(band) == 0
+    dth = np.diff(th[perm])[same]
+    assert np.all(dth > -2.0 * 2.0 * np.pi / 2**27), "angle order violated within a slab"
+
+
+def test_sorted_vertex_order_full_size_equals_default(rhg):
+    """Config 3 (n = 1e7, kbar = 100): the vertex_order = 1 graph relabelled through
+    perm is the default graph, edge for edge (compared on the GPU)."""
+    n, kbar, gamma, seed = CONFIGS[3]
+    a = rhg.generate(n, kbar, gamma, seed, "csr")
+    b = rhg.generate(n, kbar, gamma, seed, "csr", options=dict(vertex_order=1))
+    assert a.num_edges == b.num_edges
+    perm = b.perm.long()
+
+    def keys(g, p):
+        deg = torch.diff(g.row_ptr)
+        u = torch.repeat_interleave(torch.arange(n, device=deg.device), deg)
+        v = g.col.long() & 0xFFFFFFFF
+        if p is not None:
+            u, v = p[u], p[v]
+        del deg
+        return torch.sort(u * n + v).values
+
+    ka = keys(a, None)
+    del a
+    kb = keys(b, perm)
+    assert torch.equal(ka, kb)
