@@ -615,7 +615,11 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   if (gbeg + g >= gend) return;
   const uint32_t idx = (gbeg + g) * 32u + lane;
   const bool valid = idx < nlight;
+#ifdef RHG_SLAB_MAJOR  // experiment: query in sorted (slab-major) order
+  const uint32_t k = valid ? A.lay->heavy_end + idx : 0u;
+#else
   const uint32_t k = valid ? __ldg(A.order + idx) : 0u;
+#endif
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
   const uint64_t keep = policy_keep();
   const double T4 = bc.T4;
@@ -633,10 +637,16 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   const double qinv4s = inv4s_of(q.s);
   const double q4s = 4.0 * q.s;
 
+  // rows.  Sample ids: slab by slab, certain ids then hits, all through the
+  // shared-memory ring.  Sequential ids: [certain ids, slab by slab][hits, slab by
+  // slab]; the certain part through the sector registers, hits stored one by one
+  // from hcur (the count pass left the certain count in cdeg).
   RowWriter<FMT> rw;
   SecWriter<FMT> sw;
+  unsigned long long hcur = 0;
   if (MODE != QM_COUNT) {
     const unsigned long long pos0 = valid ? A.offs[qid] : 0ull;
+    if (SEQ) hcur = valid ? pos0 + A.cdeg[qid] : 0ull;
     if (SEQ) {
       sw.init(pos0, qid);
     } else {
@@ -755,7 +765,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
             const uint32_t i = wb + (uint32_t)(__ffs(m) - 1) - bp0;
             m &= m - 1u;
             const uint32_t p = pa + i + (i >= thr ? hl : 0u);
-            if (SEQ) sw.put(A, seq_id(p, bstart, nj));
+            if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
             else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
           }
         }
@@ -791,10 +801,9 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
             else over = true;
             word = 0;
           }
-        } else if (SEQ) {
-          if (hit) sw.put(A, seq_id(p, bstart, nj));
         } else if (hit) {
-          rw.put(A, qid, ld_keep(A.sid2 + p, keep));
+          if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
+          else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
         }
       }
     };
@@ -807,7 +816,11 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     }
   }
   if (MODE == QM_COUNT) {
-    if (valid) A.deg[A.labels ? k : __ldg(A.sid + k)] = deg;
+    if (valid) {
+      const uint32_t id = A.labels ? k : __ldg(A.sid + k);
+      A.deg[id] = deg;
+      if (A.labels) A.cdeg[id] = (uint32_t)certain;
+    }
     const bool anyover = __any_sync(FULL, over);
     if (lane == 0) {
       A.warp_over[g] = anyover ? 1u : 0u;

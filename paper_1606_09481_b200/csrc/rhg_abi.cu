@@ -118,7 +118,7 @@ rhg_status make_band_const(uint64_t n, double R, const rhg_options* opt, BandCon
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, sid2, dir, deg, offs,
+  size_t theta, r, keys_a, vals_a, keys_b, vals_b, sort_tmp, hist, lay, pts, sid2, dir, deg, cdeg, offs,
       scan_tmp, heavy_scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
   size_t h_pstart, h_plen, h_poff, h_np, h_vtot, h_vtot_off, h_cc,
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
@@ -164,6 +164,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.sid2 = take(2 * 4 * n);
   L.dir = take(4 * (8 * n + 4 * kMaxBands + 8));  // <= 8 n_j + 1 entries per band
   L.deg = take(4 * n);
+  L.cdeg = take(4 * n);
   L.offs = take(8 * (n + 1));
   {
     uint64_t m = n;
@@ -393,6 +394,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.bits = (uint32_t*)(ws + Lw.b_bits);
   qa.warp_over = (uint32_t*)(ws + Lw.b_over);
   qa.deg = deg;
+  qa.cdeg = (uint32_t*)(ws + Lw.cdeg);
   qa.sc = sc;
   if (bc.nshards > 1) CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of other shards stay empty
   HeavyArgs ha{};

@@ -116,6 +116,7 @@ struct QueryArgs {
   const BandLayout* __restrict__ lay;
   const uint32_t* __restrict__ order; // light query order: sorted positions, sector-major [n - heavy_end]
   uint32_t* deg;                      // count pass: degree per vertex id
+  uint32_t* cdeg;                     // count pass: certain (untested) edges per light vertex id
   const uint64_t* __restrict__ offs;  // emit pass: output offset per vertex id
   uint32_t* col;                      // CSR output
   uint32_t* pairs;                    // undirected output
