@@ -248,8 +248,11 @@ def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspac
     for attempt in range(2):
         nbytes = int(lib().rhg_workspace_bytes(n, f, cap, int(host_buffers), ctypes.byref(opts)))
         wbuf = ws.get(nbytes)
+        perm = None
         if out_bufs is not None:
-            row_ptr, col, pairs, theta, r = out_bufs(cap)
+            b = out_bufs(cap)
+            row_ptr, col, pairs, theta, r = b[:5]
+            perm = b[5] if len(b) > 5 else None
         else:
             kw = dict(device="cpu", pin_memory=True) if host_buffers else dict(device=device)
             row_ptr = torch.empty(n + 1, dtype=torch.int64, **kw) if f == RHG_CSR else None
@@ -257,8 +260,7 @@ def _run(call, n, fmt, kbar_hint, *, device, capacity, options, timing, workspac
             pairs = torch.empty((max(cap, 1), 2), dtype=torch.int32, **kw) if f != RHG_CSR else None
             theta = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
             r = torch.empty(n, dtype=torch.float64, **kw) if (want_points and sample) else None
-        perm = None
-        if opts.vertex_order == 1:
+        if opts.vertex_order == 1 and perm is None:
             kw = dict(device="cpu", pin_memory=True) if host_buffers else dict(device=device)
             perm = torch.empty(n, dtype=torch.int32, **kw)
         ne = ctypes.c_uint64()

@@ -21,20 +21,29 @@ __global__ void __launch_bounds__(RS_THREADS)
   h[threadIdx.x] = 0;
   __syncthreads();
   uint32_t base = blockIdx.x * RS_TILE;
-#pragma unroll 4
+  uint32_t kk[RS_ITEMS];
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {  // all loads in flight before the atomics
+    uint32_t i = base + it * RS_THREADS + threadIdx.x;
+    kk[it] = i < n ? __ldg(keys + i) : 0xFFFFFFFFu;
+  }
+#pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     uint32_t i = base + it * RS_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFFu], 1u);
+    if (i < n) atomicAdd(&h[(kk[it] >> shift) & 0xFFu], 1u);
   }
   __syncthreads();
   hist[threadIdx.x * G + blockIdx.x] = h[threadIdx.x];  // digit-major
 }
 
+#ifndef RHG_RS_MINB
+#define RHG_RS_MINB 3
+#endif
 // Stable scatter.  Warp w of block b owns items [b*TILE + w*512, +512) and walks
 // them in 16 rounds of 32; __match_any_sync ranks equal digits within a round.
 // The tile is then re-ordered by digit in shared memory and written out so that
 // consecutive threads store consecutive addresses of one digit run (coalesced).
-__global__ void __launch_bounds__(RS_THREADS)
+__global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     k_rs_scatter(uint32_t n, const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                  uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int shift,
                  const uint32_t* __restrict__ offs, uint32_t G) {
@@ -42,8 +51,12 @@ __global__ void __launch_bounds__(RS_THREADS)
   __shared__ uint32_t tstart[RS_RADIX];
   __shared__ uint32_t gbase[RS_RADIX];
   __shared__ uint32_t wsum[RS_WARPS];
+#ifdef RHG_RS_DIRECT
+  __shared__ uint32_t skey[1], sval[1];
+#else
   __shared__ uint32_t skey[RS_TILE];
   __shared__ uint32_t sval[RS_TILE];
+#endif
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int d = lane; d < RS_RADIX; d += 32) wcnt[w][d] = 0;
   __syncwarp();
@@ -52,11 +65,15 @@ __global__ void __launch_bounds__(RS_THREADS)
   uint32_t key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {  // all loads in flight before the ranking chain
+    const uint32_t i = wbase + it * 32 + lane;
+    key[it] = i < n ? __ldg(kin + i) : 0u;
+    val[it] = i < n ? __ldg(vin + i) : 0u;
+  }
+#pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const uint32_t i = wbase + it * 32 + lane;
     const bool valid = i < n;
-    key[it] = valid ? kin[i] : 0u;
-    val[it] = valid ? vin[i] : 0u;
     const uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     const uint32_t before = wcnt[w][d & 0xFFu];
@@ -92,6 +109,19 @@ __global__ void __launch_bounds__(RS_THREADS)
     gbase[d] = offs[d * G + blockIdx.x];
   }
   __syncthreads();
+#ifdef RHG_RS_DIRECT  // experiment: write from registers, no shared-memory reorder
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    const uint32_t i = wbase + it * 32 + lane;
+    if (i < n) {
+      const uint32_t d = (key[it] >> shift) & 0xFFu;
+      const uint32_t gp = gbase[d] + wcnt[w][d] + loc[it];
+      kout[gp] = key[it];
+      vout[gp] = val[it];
+    }
+  }
+  return;
+#endif
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const uint32_t i = wbase + it * 32 + lane;
