@@ -610,8 +610,11 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   const uint32_t nlight = A.n - A.lay->heavy_end;
   // shard: a contiguous range of the 32-vertex groups of the sector-major order
   const uint32_t ngroups = (nlight + 31u) / 32u;
-  const uint32_t gbeg = (uint32_t)shard_begin(ngroups, bc.shard, bc.nshards);
-  const uint32_t gend = (uint32_t)shard_begin(ngroups, bc.shard + 1, bc.nshards);
+  uint32_t gbeg = 0, gend = ngroups;
+  if (bc.nshards > 1) {
+    gbeg = (uint32_t)shard_begin(ngroups, bc.shard, bc.nshards);
+    gend = (uint32_t)shard_begin(ngroups, bc.shard + 1, bc.nshards);
+  }
   if (gbeg + g >= gend) return;
   const uint32_t idx = (gbeg + g) * 32u + lane;
   const bool valid = idx < nlight;
@@ -673,7 +676,20 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     SlabWin<I> w;
     w.a = w.b = w.h0 = w.h1 = w.cs = w.ce = 0;
     w.dq = 0;
-    if (on) {
+    const uint64_t wslot = ((uint64_t)g * (uint32_t)bc.L + (uint32_t)j) * 32u + (uint32_t)lane;
+    if (!WIDE && MODE == QM_EMIT_BITS && !retest && A.wc) {
+      // the count pass's window (window cache): three words per (warp, slab, lane)
+      if (on) {
+        const uint32_t a = __ldcs(A.wc + wslot), P1 = __ldcs(A.wc + A.wc_plane + wslot);
+        const uint32_t P2 = __ldcs(A.wc + 2 * A.wc_plane + wslot);
+        w.a = (I)a;
+        w.h0 = w.a + (I)(P2 & 0xFFFFu);
+        w.h1 = w.h0 + (I)(P1 & 0x7FFFFFFFu);
+        w.b = w.h1 + (I)(P2 >> 16);
+        w.cs = (P1 >> 31) ? w.b - (I)nj : w.h0;  // full window: certain [b - nj, a)
+        w.ce = (P1 >> 31) ? w.a : w.h1;
+      }
+    } else if (on) {
       const double h0 = __fma_rn(q.a, S.B0, -__dmul_rn(q.b, S.A0));
       const double h1 = __fma_rn(q.a, S.B1, -__dmul_rn(q.b, S.A1));
       const double num0 = __fma_rn(-h0, h0, T4), num1 = __fma_rn(-h1, h1, T4);
@@ -685,6 +701,16 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
         w.a = w32.a; w.b = w32.b; w.h0 = w32.h0; w.h1 = w32.h1; w.cs = w32.cs; w.ce = w32.ce;
         w.dq = w32.dq;
       }
+    }
+    if (!WIDE && MODE == QM_COUNT && A.wc) {
+      // window cache for the emit pass: a; hole = h1 - h0 (bit 31: full window with a
+      // certain arc, certain = [b - nj, a)); the two tested lengths as 16-bit halves
+      // (warps whose tests overflow their bit words re-test with fresh windows)
+      const bool fullc = w.ce > w.cs && w.h0 == w.h1;
+      __stcs(A.wc + wslot, (uint32_t)w.a);
+      __stcs(A.wc + A.wc_plane + wslot, (uint32_t)(w.h1 - w.h0) | (fullc ? 0x80000000u : 0u));
+      __stcs(A.wc + 2 * A.wc_plane + wslot,
+             ((uint32_t)(w.h0 - w.a) & 0xFFFFu) | ((uint32_t)(w.b - w.h1) << 16));
     }
     // every candidate of the warp within |dphi| < 2^-4 (300000 quanta < 2^27 2^-4 / 2pi)
     // and no window reaching across theta = 0 (so no seam pair): the short-polynomial
