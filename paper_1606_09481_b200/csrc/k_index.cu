@@ -60,10 +60,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// dir[dir_off[j] + b] = first position of band j (relative to the band start)
-// whose bucket >= b, for
+// dir[dir_off[j] + b] = first sorted position of band j whose bucket >= b, for
 // b = 0 .. nb_j (entry nb_j = band end).  Thread k fills the entries in
 // (bucket(k-1), bucket(k)]; the last point of a band also fills the tail.
+// (Radix-sorted path; the sampled path gets the directory from bucket_sort.)
 __global__ void __launch_bounds__(256)
     k_directory(uint32_t n, const uint32_t* __restrict__ skey, const BandLayout* __restrict__ lay,
                 int L, uint32_t* __restrict__ dir) {
@@ -74,11 +74,10 @@ __global__ void __launch_bounds__(256)
     uint32_t b = (key & kQMask) >> sh;
     int64_t prev = -1;
     if (k > lay->start[j]) prev = (int64_t)((skey[k - 1] & kQMask) >> sh);
-    const uint32_t rel = k - lay->start[j];
-    for (int64_t bb = prev + 1; bb <= (int64_t)b; ++bb) dir[off + bb] = rel;
+    for (int64_t bb = prev + 1; bb <= (int64_t)b; ++bb) dir[off + bb] = k;
     if (k + 1 == lay->start[j + 1]) {
       uint32_t nb = lay->nb[j];
-      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = rel + 1;
+      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
     }
   }
   // empty bands: both entries = band start
@@ -86,7 +85,7 @@ __global__ void __launch_bounds__(256)
     int j = threadIdx.x;
     if (lay->count[j] == 0) {
       uint32_t off = lay->dir_off[j], nb = lay->nb[j];
-      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = 0u;
+      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = lay->start[j];
     }
   }
 }
@@ -143,8 +142,8 @@ cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                             gen->R, skey, sidx, lay, pts, sid2, seq_ids);
   else
     k_gather<<<blocks, 256, 0, st>>>(n, theta, r, skey, sidx, lay, pts, sid2, seq_ids);
-  k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
-  if (launches) *launches += 2;
+  if (dir) k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
+  if (launches) *launches += dir ? 2 : 1;
   return cudaGetLastError();
 }
 

@@ -244,7 +244,8 @@ __device__ __forceinline__ void slab_window(int j, const BandConst& bc, const Ba
   const uint32_t lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
   auto P = [&](I bu) -> I {  // bu >> lgnb is -1, 0 or 1
     const I per = bu >> lgnb;
-    return (I)__ldg(dir + off + ((uint32_t)bu & nbm)) + (per < 0 ? -nj : (per > 0 ? nj : (I)0));
+    return (I)(__ldg(dir + off + ((uint32_t)bu & nbm)) - bstart) +
+           (per < 0 ? -nj : (per > 0 ? nj : (I)0));
   };
   I ls = 0, re = 0, cs = 0, ce = 0;
   if (!full) {
@@ -316,7 +317,7 @@ __device__ __forceinline__ void win32(const SlabC& S, int32_t q, double num, dou
   const uint32_t sh = S.sh, lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
   const uint32_t* __restrict__ D = dir + S.off;
   auto P = [&](int32_t bu) -> int32_t {  // unwrapped bucket -> unwrapped position
-    return (int32_t)__ldg(D + ((uint32_t)bu & nbm)) + (bu >> lgnb) * nj;
+    return (int32_t)(__ldg(D + ((uint32_t)bu & nbm)) - S.start) + (bu >> lgnb) * nj;
   };
   int32_t ls = P((q - d_o) >> sh), re = P(((q + d_o) >> sh) + 1);
   full = full || (re - ls >= nj);

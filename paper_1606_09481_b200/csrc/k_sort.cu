@@ -234,20 +234,42 @@ __global__ void __launch_bounds__(SC_THREADS)
   n = dev_count(n, n_dev);
   if ((uint64_t)blockIdx.x * SC_CHUNK >= n) return;
   uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK + (uint64_t)threadIdx.x * SC_ITEMS;
+  // whole 32-byte runs of the input (and 16-byte aligned output) move as vectors
+  const bool vec = sizeof(TIn) == 4 && base + SC_ITEMS <= n && ((uintptr_t)(in + base) & 15) == 0 &&
+                   ((uintptr_t)(out + base) & 15) == 0;
   TAcc v[SC_ITEMS];
   TAcc s = 0;
+  if (vec) {
+    const uint4 a = reinterpret_cast<const uint4*>(in + base)[0];
+    const uint4 b = reinterpret_cast<const uint4*>(in + base)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
 #pragma unroll
-  for (int it = 0; it < SC_ITEMS; ++it) {
-    uint64_t i = base + it;
-    v[it] = i < n ? (TAcc)in[i] : TAcc(0);
-    s += v[it];
+    for (int it = 0; it < SC_ITEMS; ++it) {
+      uint64_t i = base + it;
+      v[it] = i < n ? (TAcc)in[i] : TAcc(0);
+    }
   }
+#pragma unroll
+  for (int it = 0; it < SC_ITEMS; ++it) s += v[it];
   TAcc ex = block_excl_scan<TAcc>(s, sh, (TAcc*)nullptr) + partial[blockIdx.x];
+  TOut o[SC_ITEMS];
 #pragma unroll
   for (int it = 0; it < SC_ITEMS; ++it) {
-    uint64_t i = base + it;
-    if (i < n) out[i] = (TOut)ex;
+    o[it] = (TOut)ex;
     ex += v[it];
+  }
+  if (vec) {
+    uint4* d = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+    for (int q = 0; q < (int)(SC_ITEMS * sizeof(TOut) / 16); ++q) d[q] = reinterpret_cast<const uint4*>(o)[q];
+  } else {
+#pragma unroll
+    for (int it = 0; it < SC_ITEMS; ++it) {
+      uint64_t i = base + it;
+      if (i < n) out[i] = o[it];
+    }
   }
 }
 

@@ -124,7 +124,7 @@ struct Layout {
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
   size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off, wc;
   uint64_t wc_plane;
-  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps;
+  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps, dir_cap;
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
@@ -164,7 +164,8 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.lay = take(sizeof(BandLayout));
   L.pts = take(2 * sizeof(PointRec) * n);  // doubled SoA
   L.sid2 = take(2 * 4 * n);
-  L.dir = take(4 * (8 * n + 4 * kMaxBands + 8));  // <= 8 n_j + 1 entries per band
+  L.dir_cap = 8 * n + 4 * kMaxBands + 8;  // <= 8 n_j + 1 entries per band
+  L.dir = take(4 * L.dir_cap);
   L.deg = take(4 * n);
   L.cdeg = take(4 * n);
   L.offs = take(8 * (n + 1));
