@@ -314,10 +314,11 @@ __device__ __forceinline__ void win32(const SlabC& S, int32_t q, double num, dou
   const int32_t d_i =
       certok ? (int32_t)(sqrt_approx(rf1) * (2.0f * (float)RHG_Q27_SCALE * 0.99999237060546875f)) - 1
              : -1;
-  const uint32_t sh = S.sh, lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u;
-  const uint32_t* __restrict__ D = dir + S.off;
-  auto P = [&](int32_t bu) -> int32_t {  // unwrapped bucket -> unwrapped position
-    return (int32_t)(__ldg(D + ((uint32_t)bu & nbm)) - S.start) + (bu >> lgnb) * nj;
+  const uint32_t sh = S.sh, lgnb = kQBits - sh, nbm = (1u << lgnb) - 1u, off = S.off;
+  const int32_t mstart = -(int32_t)S.start;
+  auto P = [&](int32_t bu) -> int32_t {  // unwrapped bucket -> unwrapped slab position
+    const uint32_t e = off + ((uint32_t)bu & nbm);  // 32-bit index: one wide IMAD address
+    return (int32_t)__ldg(dir + e) + (bu >> lgnb) * nj + mstart;
   };
   int32_t ls = P((q - d_o) >> sh), re = P(((q + d_o) >> sh) + 1);
   full = full || (re - ls >= nj);

@@ -514,3 +514,30 @@ def test_sorted_vertex_order_full_size_equals_default(rhg):
     del a
     kb = keys(b, perm)
     assert torch.equal(ka, kb)
+
+
+def test_sorted_vertex_order_host_buffers_and_shards(rhg):
+    """vertex_order = 1 through host buffers (perm copied to the host) and sharded:
+    identical to the device-buffer, unsharded call."""
+    n, kbar, gamma, seed = CONFIGS[4]
+    o = dict(vertex_order=1)
+    gd = rhg.generate(n, kbar, gamma, seed, "csr", options=o)
+    gh = rhg.generate(n, kbar, gamma, seed, "csr", options=o, host_buffers=True)
+    assert not gh.perm.is_cuda
+    assert torch.equal(gh.perm, gd.perm.cpu())
+    assert torch.equal(gh.row_ptr, gd.row_ptr.cpu()) and torch.equal(gh.col, gd.col.cpu())
+    N = 2
+    parts = [rhg.generate(n, kbar, gamma, seed, "csr",
+                          options=dict(o, shard_index=s, shard_count=N)) for s in range(N)]
+    assert sum(p.num_edges for p in parts) == gd.num_edges
+    rp, col = gd.row_ptr.cpu().numpy(), gd.col.cpu().numpy()
+    deg_sum = np.zeros(n, dtype=np.int64)
+    for p in parts:
+        assert torch.equal(p.perm, gd.perm)
+        prp, pcol = p.row_ptr.cpu().numpy(), p.col.cpu().numpy()
+        d = np.diff(prp)
+        deg_sum += d
+        own = np.nonzero(d)[0]
+        for v in own[:: max(1, len(own) // 300)]:
+            assert np.array_equal(pcol[prp[v]:prp[v + 1]], col[rp[v]:rp[v + 1]])
+    assert np.array_equal(deg_sum, np.diff(rp))
