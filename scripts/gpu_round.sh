@@ -7,7 +7,7 @@ O=gpurun_out
 nvidia-smi > $O/smi.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench exit $?" >> $O/bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $O/ncu_launch.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-configs > $O/ncu_launch.log 2>&1
 for o in 1 0; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_(query|heavy)$" -c 4 \
     -o $O/kq_o${o} -f python scripts/prof_step.py --cfg 3 --reps 1 --order $o > $O/kq_o${o}.log 2>&1
