@@ -410,40 +410,63 @@ __device__ __forceinline__ uint32_t lane_range_mask(int lo, int hi) {
 //                  some lane needs more than kLightBitRows words)
 //   QM_EMIT      : writes the rows, re-testing
 //   QM_EMIT_BITS : writes the rows, replaying the bits (re-tests warps with warp_over)
-constexpr int kStageStride = 17;  // 16-word ring per lane (+1: bank-conflict-free)
+constexpr int kStageStride = 16;  // 16-word ring per lane, 16-byte groups XOR-swizzled by lane
 
 template <int FMT>
 struct RowWriter {
   // CSR: 8 ids per 32-byte sector; pairs: 4 (u, v) pairs per sector.  The stage is
   // a two-sector ring; a sector goes out (one STG.256) when the next one starts.
+  // Word w of the ring lives at w ^ sw (sw flips bits 2-3 by lane: 16-byte groups
+  // stay whole, so a sector is read back with two LDS.128).
   static constexpr uint32_t EPS = FMT == RHG_CSR ? 8u : 4u;
-  uint32_t* stage;                 // this lane's ring (16 words)
+  uint32_t* stage;                 // this lane's ring (16 words, 64-byte aligned)
+  uint32_t sw;                     // swizzle
   unsigned long long pos, start;   // next slot, first slot of the row (elements)
   __device__ __forceinline__ void store_elem(uint32_t slot, uint32_t vid, uint32_t w) {
     if (FMT == RHG_CSR) {
-      stage[slot] = w;
+      stage[slot ^ sw] = w;
     } else {
-      stage[2 * slot] = vid < w ? vid : w;
-      stage[2 * slot + 1] = vid < w ? w : vid;
+      *reinterpret_cast<uint2*>(stage + ((2 * slot) ^ sw)) =
+          vid < w ? make_uint2(vid, w) : make_uint2(w, vid);
     }
   }
-  __device__ __forceinline__ void write_elems(const QueryArgs& A, unsigned long long s0,
-                                              const uint32_t* r, uint32_t lo, uint32_t hi) {
-    for (uint32_t x = lo; x < hi; ++x) {
-      if (FMT == RHG_CSR) A.col[s0 + x] = r[x];
-      else reinterpret_cast<uint2*>(A.pairs)[s0 + x] = make_uint2(r[2 * x], r[2 * x + 1]);
+  // words [8 h + a, 8 h + a + k) of the ring (k = 1, 2, 4; a a multiple of k) -> dst
+  __device__ __forceinline__ void store_words(uint32_t* dst, uint32_t h, uint32_t a, uint32_t k) {
+    const uint32_t* src = stage + ((8u * h + a) ^ sw);
+    if (k == 4) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    else if (k == 2) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(src);
+    else *dst = *src;
+  }
+  // elements [lo, hi) of the sector in ring half h (a partial sector: the first or
+  // last of the row) with at most five aligned vector stores
+  __device__ __forceinline__ void store_range(const QueryArgs& A, unsigned long long s0, uint32_t h,
+                                              uint32_t lo, uint32_t hi) {
+    uint32_t* base = FMT == RHG_CSR ? A.col + s0 : A.pairs + 2 * s0;
+    uint32_t x = lo;
+    if (FMT == RHG_CSR) {
+      if ((x & 1u) && x < hi) { store_words(base + x, h, x, 1); x += 1; }
+      if ((x & 2u) && x + 2u <= hi) { store_words(base + x, h, x, 2); x += 2; }
+      if (x + 4u <= hi) { store_words(base + x, h, x, 4); x += 4; }
+      if (x + 2u <= hi) { store_words(base + x, h, x, 2); x += 2; }
+      if (x < hi) store_words(base + x, h, x, 1);
+    } else {  // element = one (u, v) pair, two words
+      if ((x & 1u) && x < hi) { store_words(base + 2 * x, h, 2 * x, 2); x += 1; }
+      if (x + 2u <= hi) { store_words(base + 2 * x, h, 2 * x, 4); x += 2; }
+      if (x < hi) store_words(base + 2 * x, h, 2 * x, 2);
     }
   }
   __device__ __forceinline__ void flush(const QueryArgs& A, unsigned long long sec) {
-    const uint32_t* r = stage + (uint32_t)(sec & 1) * 8u;
+    const uint32_t h = (uint32_t)(sec & 1);
     const unsigned long long s0 = sec * EPS;
     if (s0 >= start) {
       uint32_t* dst = FMT == RHG_CSR ? A.col + s0 : A.pairs + 2 * s0;
-      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]),
-                   "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      const uint4 a = *reinterpret_cast<const uint4*>(stage + ((8u * h) ^ sw));
+      const uint4 b = *reinterpret_cast<const uint4*>(stage + ((8u * h + 4u) ^ sw));
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(a.x),
+                   "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                    : "memory");
     } else {  // first sector of the row: the slots before `start` belong to the previous row
-      write_elems(A, s0, r, (uint32_t)(start - s0), EPS);
+      store_range(A, s0, h, (uint32_t)(start - s0), EPS);
     }
   }
   // append w[lo..hi) (hi - lo <= 4 < 2 EPS)
@@ -466,7 +489,7 @@ struct RowWriter {
     const uint32_t x = (uint32_t)pos & (EPS - 1);
     if (x) {
       const unsigned long long sec = pos / EPS, s0 = sec * EPS;
-      write_elems(A, s0, stage + (uint32_t)(sec & 1) * 8u, s0 >= start ? 0u : (uint32_t)(start - s0), x);
+      store_range(A, s0, (uint32_t)(sec & 1), s0 >= start ? 0u : (uint32_t)(start - s0), x);
     }
   }
 };
@@ -588,7 +611,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
   __shared__ BandSm bs;
   __shared__ SlabC scs[kMaxBands];
-  __shared__ uint32_t stage_all[(MODE == QM_COUNT || SEQ) ? 1 : QK_THREADS * kStageStride];
+  __shared__ __align__(16) uint32_t stage_all[(MODE == QM_COUNT || SEQ) ? 4 : QK_THREADS * kStageStride];
   load_band_sm(bs, A.lay, bc.L);
   if (threadIdx.x < (unsigned)bc.L) {
     const int j = threadIdx.x;
@@ -656,6 +679,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
       sw.init(pos0, qid);
     } else {
       rw.stage = stage_all + threadIdx.x * kStageStride;
+      rw.sw = ((threadIdx.x >> 1) & 3u) << 2;
       rw.pos = rw.start = pos0;
     }
   }
