@@ -1087,6 +1087,12 @@ __global__ void __launch_bounds__(HV_THREADS, 4)
         uint32_t m;
         if (MODE == QM_EMIT_BITS && bits) {
           m = H.bits[wbase + bt];
+        } else if (!__any_sync(FULL, act && !o_cert)) {
+          // a batch of certain candidates only (hub rows are mostly certain): no loads,
+          // no tests
+          m = __ballot_sync(FULL, act);
+          if (MODE == QM_COUNT && bits && lane == 0) H.bits[wbase + bt] = m;
+          if (MODE == QM_COUNT) cert_total += __popc(m);
         } else {
           const bool test = act && !o_cert;
           const double2* xp = reinterpret_cast<const double2*>(A.pts + (test ? p : 0u));
