@@ -6,6 +6,16 @@
 
 namespace rhg {
 
+__device__ __forceinline__ uint32_t warp_incl_u32(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += a;
+  }
+  return v;
+}
+
 // Point record for sorted position k: theta, sinh r, e^{r/2}, e^{-r/2}.
 // (cosh d - 1 = 2 sinh^2((r_p - r_q)/2) + 2 sinh r_p sinh r_q sin^2(dphi/2), and
 //  2 sinh((r_p - r_q)/2) = e^{r_p/2} e^{-r_q/2} - e^{-r_p/2} e^{r_q/2}.)
@@ -67,25 +77,59 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_directory(uint32_t n, const uint32_t* __restrict__ skey, const BandLayout* __restrict__ lay,
                 int L, uint32_t* __restrict__ dir) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    uint32_t key = skey[k];
-    uint32_t j = key >> kBandShift;
-    uint32_t sh = lay->shift[j], off = lay->dir_off[j];
-    uint32_t b = (key & kQMask) >> sh;
-    int64_t prev = -1;
-    if (k > lay->start[j]) prev = (int64_t)((skey[k - 1] & kQMask) >> sh);
-    for (int64_t bb = prev + 1; bb <= (int64_t)b; ++bb) dir[off + bb] = k;
-    if (k + 1 == lay->start[j + 1]) {
-      uint32_t nb = lay->nb[j];
-      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
+  // Warp-cooperative: the entries owned by 32 consecutive points are one contiguous
+  // stretch of the directory (per band), written 32 consecutive entries per store
+  // instruction.  Point k owns (bucket(k-1), bucket(k)] (value k); the last point
+  // of a band also owns (bucket(k), nb_j] (value k + 1, written by its lane).
+  __shared__ uint8_t tbl[8][32];
+  __shared__ uint2 own[8][32];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + wi; (uint64_t)w * 32 < n; w += nwarps) {
+    const uint32_t k = w * 32 + (uint32_t)lane;
+    uint32_t len = 0, base = 0, j = 0, b = 0;
+    if (k < n) {
+      const uint32_t key = __ldg(skey + k);
+      j = key >> kBandShift;
+      const uint32_t sh = lay->shift[j], off = lay->dir_off[j];
+      b = (key & kQMask) >> sh;
+      uint32_t first = 0;  // first entry I own
+      if (k > lay->start[j]) first = ((__ldg(skey + k - 1) & kQMask) >> sh) + 1;
+      len = b + 1 - first;  // 0 if the previous point shares my bucket
+      base = off + first;
+      if (k + 1 == lay->start[j + 1]) {  // band tail: (b, nb] -> k + 1
+        const uint32_t nb = lay->nb[j];
+        for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
+      }
     }
+    const uint32_t incl = warp_incl_u32(len), T = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t pre = incl - len;
+    const uint32_t NE = __ballot_sync(0xffffffffu, len > 0);
+    if (len > 0) {
+      tbl[wi][__popc(NE & ((1u << lane) - 1u))] = (uint8_t)lane;
+      own[wi][lane] = make_uint2(base - pre, k);  // entry t -> dir[base - pre + t] = k
+    }
+    __syncwarp();
+    uint32_t R0 = 0;
+    for (uint32_t B = 0; B < T; B += 32) {
+      const uint32_t sb = pre - B;
+      const uint32_t M = __reduce_or_sync(0xffffffffu, (len > 0 && sb < 32u) ? (1u << sb) : 0u);
+      const uint32_t rank = R0 + __popc(M & (0xffffffffu >> (31 - lane)));
+      R0 += __popc(M);
+      const uint32_t t = B + (uint32_t)lane;
+      if (t < T) {
+        const uint2 o = own[wi][tbl[wi][(rank - 1u) & 31u]];
+        dir[o.x + t] = o.y;
+      }
+    }
+    __syncwarp();
   }
   // empty bands: both entries = band start
   if (blockIdx.x == 0 && threadIdx.x < (unsigned)L) {
-    int j = threadIdx.x;
-    if (lay->count[j] == 0) {
-      uint32_t off = lay->dir_off[j], nb = lay->nb[j];
-      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = lay->start[j];
+    int jj = threadIdx.x;
+    if (lay->count[jj] == 0) {
+      uint32_t off = lay->dir_off[jj], nb = lay->nb[jj];
+      for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = lay->start[jj];
     }
   }
 }
