@@ -26,14 +26,16 @@
 //    Z13) is one contiguous index range: per (vertex, slab) the candidates are
 //    one range [a, b) with the certain sub-range [h0, h1) cut out of it.
 //
-// Work decomposition (B200): one warp owns 32 consecutive query vertices (same
-// slab, neighbouring angles: their candidate ranges overlap, so the point SoA is
-// read from L2, not HBM, once per neighbourhood).  Per slab each lane computes
-// its vertex's ranges; the warp then walks the concatenation of the 32 lanes'
-// ranges 32 candidates at a time, so every lane tests a candidate in every batch
-// whatever the range lengths.  The owner of a candidate is found with one
-// warp-wide OR of segment-start bits and a popcount (no search).  Hub vertices
-// take the chunked path at the end of this file.
+// Work decomposition (B200): one warp owns 32 consecutive entries of the
+// sector-major query order (same slab and angular sector: their candidate ranges
+// overlap, so the point SoA is read from L2, not HBM, about once per pass); lane =
+// vertex, slabs in lock step.  Per slab each lane computes its vertex's window and
+// walks its own candidates: the count pass tests the annulus and stores one bit per
+// test; the emit pass recomputes the window, writes the certain ids and replays
+// the set bits.  Rows leave the SM in whole 32-byte sectors (a shared-memory ring
+// for sample ids, eight sector registers for sequential ids).  Hub vertices take
+// the chunked path at the end of this file.  DESIGN.md §7 lists the layouts that
+// were measured against this one.
 #include <cstdio>
 #include <type_traits>
 
@@ -62,7 +64,6 @@ namespace rhg {
 constexpr int QK_WARPS = 4;
 constexpr int QK_THREADS = QK_WARPS * 32;
 constexpr uint32_t FULL = 0xffffffffu;
-constexpr uint32_t NO_BLOCK = 0xffffffffu;
 
 // test range of one owner lane (indexed by its rank among the lanes with tests):
 // candidate t (flattened index) -> doubled position aoff + t (+ hlen past thr)
@@ -375,19 +376,11 @@ __device__ __forceinline__ uint32_t ld_keep(const uint32_t* ptr, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
   return v;
 }
-constexpr int kCopyUnroll = 4;
 
 template <int FMT>
 __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long long o, uint32_t vid,
                                            uint32_t w) {
   RHG_CHECK(o < A.out_cap);
-#if defined(RHG_EXP) && RHG_EXP == 1  // experiment: no output stores (loads kept alive)
-  if (w == 0xFFFFFFFFu && o == 0) A.col[0] = w;
-  return;
-#elif defined(RHG_EXP) && RHG_EXP == 3  // experiment: every thread stores to its own slot
-  A.col[(blockIdx.x * blockDim.x + threadIdx.x) & 0xFFFFFu] = w;
-  return;
-#endif
   if (FMT == RHG_CSR) A.col[o] = w;
   else reinterpret_cast<uint2*>(A.pairs)[o] = vid < w ? make_uint2(vid, w) : make_uint2(w, vid);
 }
@@ -643,11 +636,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   if (gbeg + g >= gend) return;
   const uint32_t idx = (gbeg + g) * 32u + lane;
   const bool valid = idx < nlight;
-#ifdef RHG_SLAB_MAJOR  // experiment: query in sorted (slab-major) order
-  const uint32_t k = valid ? A.lay->heavy_end + idx : 0u;
-#else
   const uint32_t k = valid ? __ldg(A.order + idx) : 0u;
-#endif
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
   const uint64_t keep = policy_keep();
   const double T4 = bc.T4;
@@ -702,20 +691,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     SlabWin<I> w;
     w.a = w.b = w.h0 = w.h1 = w.cs = w.ce = 0;
     w.dq = 0;
-    const uint64_t wslot = ((uint64_t)g * (uint32_t)bc.L + (uint32_t)j) * 32u + (uint32_t)lane;
-    if (!WIDE && MODE == QM_EMIT_BITS && !retest && A.wc) {
-      // the count pass's window (window cache): three words per (warp, slab, lane)
-      if (on) {
-        const uint32_t a = __ldcs(A.wc + wslot), P1 = __ldcs(A.wc + A.wc_plane + wslot);
-        const uint32_t P2 = __ldcs(A.wc + 2 * A.wc_plane + wslot);
-        w.a = (I)a;
-        w.h0 = w.a + (I)(P2 & 0xFFFFu);
-        w.h1 = w.h0 + (I)(P1 & 0x7FFFFFFFu);
-        w.b = w.h1 + (I)(P2 >> 16);
-        w.cs = (P1 >> 31) ? w.b - (I)nj : w.h0;  // full window: certain [b - nj, a)
-        w.ce = (P1 >> 31) ? w.a : w.h1;
-      }
-    } else if (on) {
+    if (on) {
       const double h0 = __fma_rn(q.a, S.B0, -__dmul_rn(q.b, S.A0));
       const double h1 = __fma_rn(q.a, S.B1, -__dmul_rn(q.b, S.A1));
       const double num0 = __fma_rn(-h0, h0, T4), num1 = __fma_rn(-h1, h1, T4);
@@ -727,16 +703,6 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
         w.a = w32.a; w.b = w32.b; w.h0 = w32.h0; w.h1 = w32.h1; w.cs = w32.cs; w.ce = w32.ce;
         w.dq = w32.dq;
       }
-    }
-    if (!WIDE && MODE == QM_COUNT && A.wc) {
-      // window cache for the emit pass: a; hole = h1 - h0 (bit 31: full window with a
-      // certain arc, certain = [b - nj, a)); the two tested lengths as 16-bit halves
-      // (warps whose tests overflow their bit words re-test with fresh windows)
-      const bool fullc = w.ce > w.cs && w.h0 == w.h1;
-      __stcs(A.wc + wslot, (uint32_t)w.a);
-      __stcs(A.wc + A.wc_plane + wslot, (uint32_t)(w.h1 - w.h0) | (fullc ? 0x80000000u : 0u));
-      __stcs(A.wc + 2 * A.wc_plane + wslot,
-             ((uint32_t)(w.h0 - w.a) & 0xFFFFu) | ((uint32_t)(w.b - w.h1) << 16));
     }
     // every candidate of the warp within |dphi| < 2^-4 (300000 quanta < 2^27 2^-4 / 2pi)
     // and no window reaching across theta = 0 (so no seam pair): the short-polynomial

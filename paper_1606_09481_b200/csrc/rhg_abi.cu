@@ -122,13 +122,11 @@ struct Layout {
       scan_tmp, heavy_scan_tmp, sc, st_rowptr, st_edges, st_in_theta, st_in_r, bits, total;
   size_t h_pstart, h_plen, h_poff, h_np, h_vtot, h_vtot_off, h_cc,
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
-  size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off, wc;
-  uint64_t wc_plane;
+  size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
   uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps, dir_cap;
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
-constexpr uint64_t kWindowCacheMax = 8ull << 30;  // bytes
 constexpr uint64_t kChunkMin = 1024;
 
 int bands_for(uint64_t n, const rhg_options* opt) {
@@ -192,12 +190,6 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.h_bits = take(4 * L.hbits_cap);
   L.b_bits = take(4ull * kLightBitRows * 32 * L.light_warps);
   L.b_over = take(4 * L.light_warps);
-  // window cache (count -> emit, 12 B per light vertex and slab), when it stays small
-  L.wc_plane = L.light_warps * (uint64_t)nbands * 32ull;
-  L.wc = 0;
-#ifdef RHG_WINDOW_CACHE  // experiment (measured slower: 1.9 GB of extra traffic at config 3)
-  if (n < (1ull << 30) && 12ull * L.wc_plane <= kWindowCacheMax) L.wc = take(12ull * L.wc_plane);
-#endif
   L.q_order = take(4 * n);
   L.q_cell_lo = take(4 * kQuerySectors * kMaxBands);
   L.q_cell_cnt = take(4 * kQuerySectors * kMaxBands);
@@ -402,8 +394,6 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.order = (const uint32_t*)(ws + Lw.q_order);
   qa.bits = (uint32_t*)(ws + Lw.b_bits);
   qa.warp_over = (uint32_t*)(ws + Lw.b_over);
-  qa.wc = Lw.wc ? (uint32_t*)(ws + Lw.wc) : nullptr;
-  qa.wc_plane = Lw.wc_plane;
   qa.deg = deg;
   qa.cdeg = (uint32_t*)(ws + Lw.cdeg);
   qa.sc = sc;

@@ -125,8 +125,6 @@ struct QueryArgs {
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
   uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
-  uint32_t* wc;                       // window cache, 3 planes of wc_plane words (or null)
-  uint64_t wc_plane;                  // light warps x L x 32
 };
 
 // Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.
