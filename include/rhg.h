@@ -81,7 +81,10 @@ typedef struct {
      rhg_output.perm_out, if set, receives perm[id] = sample / input index.
      theta_out / r_out stay in sample order. */
   int vertex_order;
-  int reserved[2];
+  /* 1: run the light query kernels with 64-bit slab positions even when every slab
+     holds < 2^30 points (the path n >= 2^30 takes; a test knob, same output). */
+  int wide_positions;
+  int reserved[1];
 } rhg_options;
 
 /* Per-phase device times (CUDA events on the caller's stream), filled when

@@ -1134,7 +1134,8 @@ cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
   const uint32_t groups = ((qa.n + 31) / 32 + bc.nshards - 1) / bc.nshards + 1;
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
-  const bool wide = qa.n >= (1u << 30);  // a slab may hold >= 2^30 points: 64-bit positions
+  // a slab may hold >= 2^30 points: 64-bit positions (or forced, rhg_options.wide_positions)
+  const bool wide = qa.n >= (1u << 30) || qa.force_wide;
 #define RHG_LQ(M, F, S)                                                                \
   do {                                                                                 \
     if (wide) k_query<M, F, true, S><<<blocks, QK_THREADS, 0, st>>>(qa, bc);           \

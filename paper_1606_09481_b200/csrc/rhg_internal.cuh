@@ -125,6 +125,7 @@ struct QueryArgs {
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
   uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
+  uint32_t force_wide;                // 64-bit slab positions in the light kernels
 };
 
 // Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.

@@ -541,3 +541,20 @@ def test_sorted_vertex_order_host_buffers_and_shards(rhg):
         for v in own[:: max(1, len(own) // 300)]:
             assert np.array_equal(pcol[prp[v]:prp[v + 1]], col[rp[v]:rp[v + 1]])
     assert np.array_equal(deg_sum, np.diff(rp))
+
+
+@pytest.mark.parametrize("fmt,order", [("csr", 0), ("pairs", 0), ("csr", 1)])
+def test_wide_positions_path_matches(rhg, fmt, order):
+    """The 64-bit-position light kernels (taken for n >= 2^30, which does not fit one
+    GPU's memory) forced at config 4: identical output to the 32-bit path."""
+    n, kbar, gamma, seed = CONFIGS[4]
+    a = rhg.generate(n, kbar, gamma, seed, fmt, options=dict(vertex_order=order))
+    b = rhg.generate(n, kbar, gamma, seed, fmt, options=dict(vertex_order=order, wide_positions=1))
+    assert a.num_edges == b.num_edges
+    if fmt == "csr":
+        assert torch.equal(a.row_ptr, b.row_ptr)
+        ka = csr_checked_pairs(a)
+        kb = csr_checked_pairs(b)
+    else:
+        ka, kb = pairs_checked(a), pairs_checked(b)
+    assert np.array_equal(ka, kb)
