@@ -14,53 +14,78 @@ constexpr int RS_ITEMS = 16;                       // per thread
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per block
 constexpr int RS_RADIX = 256;
 
+// One read of the keys: the digit histograms of all passes (shift 8 p, p < P).
 __global__ void __launch_bounds__(RS_THREADS)
-    k_rs_hist(uint32_t n, const uint32_t* __restrict__ keys, int shift, uint32_t* __restrict__ hist,
-              uint32_t G) {
-  __shared__ uint32_t h[RS_RADIX];
-  h[threadIdx.x] = 0;
+    k_rs_hist_all(uint32_t n, const uint32_t* __restrict__ keys, int P, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[4][RS_RADIX];
+  for (int p = 0; p < 4; ++p) h[p][threadIdx.x] = 0;
   __syncthreads();
-  uint32_t base = blockIdx.x * RS_TILE;
-  uint32_t kk[RS_ITEMS];
-#pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {  // all loads in flight before the atomics
-    uint32_t i = base + it * RS_THREADS + threadIdx.x;
-    kk[it] = i < n ? __ldg(keys + i) : 0xFFFFFFFFu;
-  }
-#pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    uint32_t i = base + it * RS_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&h[(kk[it] >> shift) & 0xFFu], 1u);
+  for (uint32_t i = blockIdx.x * RS_THREADS + threadIdx.x; i < n; i += gridDim.x * RS_THREADS) {
+    const uint32_t k = __ldg(keys + i);
+    for (int p = 0; p < P; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
   }
   __syncthreads();
-  hist[threadIdx.x * G + blockIdx.x] = h[threadIdx.x];  // digit-major
+  for (int p = 0; p < P; ++p)
+    if (h[p][threadIdx.x]) atomicAdd(&ghist[p * RS_RADIX + threadIdx.x], h[p][threadIdx.x]);
+}
+
+// exclusive scan of each pass's 256 digit counts -> digit start positions
+__global__ void __launch_bounds__(RS_RADIX) k_rs_digit_start(int P, const uint32_t* __restrict__ ghist,
+                                                             uint32_t* __restrict__ dstart) {
+  __shared__ uint32_t ws[RS_RADIX / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int p = 0; p < P; ++p) {
+    const uint32_t c = ghist[p * RS_RADIX + threadIdx.x];
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int ww = 0; ww < w; ++ww) pre += ws[ww];
+    dstart[p * RS_RADIX + threadIdx.x] = pre + inc - c;
+    __syncthreads();
+  }
 }
 
 #ifndef RHG_RS_MINB
 #define RHG_RS_MINB 3
 #endif
-// Stable scatter.  Warp w of block b owns items [b*TILE + w*512, +512) and walks
-// them in 16 rounds of 32; __match_any_sync ranks equal digits within a round.
-// The tile is then re-ordered by digit in shared memory and written out so that
-// consecutive threads store consecutive addresses of one digit run (coalesced).
+// Look-back status of (tile, digit): bits 62-63 flag (0 not yet, 1 tile count,
+// 2 inclusive prefix over tiles), bits 0-61 the value.
+constexpr unsigned long long kRsAgg = 1ull << 62, kRsIncl = 2ull << 62;
+constexpr unsigned long long kRsVal = (1ull << 62) - 1ull;
+
+// One LSD pass ("onesweep"): tiles take tickets in the order they start; each
+// ranks its keys by digit (warp w of the tile owns items [w*512, +512) and walks
+// them in 16 rounds of 32; __match_any_sync ranks equal digits within a round, so
+// the order is stable), publishes its per-digit counts, and finds the count of
+// every digit in all earlier tiles by decoupled look-back (thread d walks back over
+// the tiles' (tile, d) words until an inclusive prefix).  The tile is then
+// re-ordered by digit in shared memory and written out so that consecutive threads
+// store consecutive addresses of one digit run (coalesced).  A tile waits only on
+// tiles that took earlier tickets, so every wait ends.
 __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
-    k_rs_scatter(uint32_t n, const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                 uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int shift,
-                 const uint32_t* __restrict__ offs, uint32_t G) {
+    k_rs_onesweep(uint32_t n, const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                  uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int shift,
+                  const uint32_t* __restrict__ dstart, unsigned long long* status,
+                  uint32_t* ticket) {
   __shared__ uint32_t wcnt[RS_WARPS][RS_RADIX];
   __shared__ uint32_t tstart[RS_RADIX];
   __shared__ uint32_t gbase[RS_RADIX];
   __shared__ uint32_t wsum[RS_WARPS];
-#ifdef RHG_RS_DIRECT
-  __shared__ uint32_t skey[1], sval[1];
-#else
   __shared__ uint32_t skey[RS_TILE];
   __shared__ uint32_t sval[RS_TILE];
-#endif
+  __shared__ uint32_t tile_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
   for (int d = lane; d < RS_RADIX; d += 32) wcnt[w][d] = 0;
-  __syncwarp();
-  const uint32_t tbase = blockIdx.x * RS_TILE;
+  __syncthreads();
+  const uint32_t tile = tile_s;
+  const uint32_t tbase = tile * RS_TILE;
   const uint32_t wbase = tbase + w * (32 * RS_ITEMS);
   uint32_t key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
   const uint32_t lt = (1u << lane) - 1u;
@@ -84,7 +109,8 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
   }
   __syncthreads();
   // per digit: exclusive prefix over warps (warp order = item order => stable),
-  // then the digit's start inside the tile (block scan over the 256 digit totals)
+  // the digit's start inside the tile (block scan over the 256 digit totals), and
+  // its start in the output (digit start + counts of earlier tiles, look-back)
   {
     const int d = threadIdx.x;  // RS_THREADS == RS_RADIX
     uint32_t run = 0;
@@ -94,6 +120,19 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
       wcnt[ww][d] = run;
       run += c;
     }
+    volatile unsigned long long* my = status + (size_t)tile * RS_RADIX + d;
+    *my = (tile == 0 ? kRsIncl : kRsAgg) | run;
+    unsigned long long excl = 0;
+    for (uint32_t t2 = tile; t2 > 0; --t2) {
+      const volatile unsigned long long* o = status + (size_t)(t2 - 1) * RS_RADIX + d;
+      unsigned long long v;
+      do {
+        v = *o;
+      } while ((v & ~kRsVal) == 0ull);
+      excl += v & kRsVal;
+      if ((v & ~kRsVal) == kRsIncl) break;
+    }
+    if (tile) *my = kRsIncl | (excl + run);
     uint32_t inc = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -106,22 +145,9 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) wpre += (ww < w) ? wsum[ww] : 0u;
     tstart[d] = wpre + inc - run;
-    gbase[d] = offs[d * G + blockIdx.x];
+    gbase[d] = dstart[d] + (uint32_t)excl;
   }
   __syncthreads();
-#ifdef RHG_RS_DIRECT  // experiment: write from registers, no shared-memory reorder
-#pragma unroll
-  for (int it = 0; it < RS_ITEMS; ++it) {
-    const uint32_t i = wbase + it * 32 + lane;
-    if (i < n) {
-      const uint32_t d = (key[it] >> shift) & 0xFFu;
-      const uint32_t gp = gbase[d] + wcnt[w][d] + loc[it];
-      kout[gp] = key[it];
-      vout[gp] = val[it];
-    }
-  }
-  return;
-#endif
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const uint32_t i = wbase + it * 32 + lane;
@@ -298,23 +324,11 @@ cudaError_t exclusive_scan_u32_u64_dev(uint64_t n_cap, const unsigned long long*
   return cudaGetLastError();
 }
 
-static cudaError_t exclusive_scan_u32_inplace(uint32_t n, uint32_t* data, uint32_t* partial,
-                                              cudaStream_t st, int* launches) {
-  uint32_t B = sc_blocks(n);
-  k_scan_reduce<uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, partial, nullptr);
-  k_scan_partials<uint32_t, uint32_t><<<1, SC_THREADS, 0, st>>>(B, partial, (uint32_t*)nullptr, n,
-                                                                nullptr, nullptr);
-  k_scan_down<uint32_t, uint32_t, uint32_t><<<B, SC_THREADS, 0, st>>>(n, data, data, partial,
-                                                                      nullptr);
-  if (launches) *launches += 3;
-  return cudaGetLastError();
-}
-
+// tmp: digit counts and starts (4 passes x 256), tickets, look-back words
 size_t radix_sort_tmp_bytes(uint64_t n) {
   uint64_t G = (n + RS_TILE - 1) / RS_TILE;
   if (G == 0) G = 1;
-  uint64_t H = G * RS_RADIX;
-  return (size_t)(H + sc_blocks(H) + 64) * sizeof(uint32_t) + 256;
+  return (size_t)(2 * 4 * RS_RADIX + 8) * sizeof(uint32_t) + 4 * G * RS_RADIX * 8ull + 256;
 }
 
 cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
@@ -322,22 +336,28 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
                        int* launches) {
   uint32_t G = (n + RS_TILE - 1) / RS_TILE;
   if (G == 0) return cudaSuccess;
-  uint32_t* hist = (uint32_t*)tmp;
-  uint32_t* partial = hist + (size_t)G * RS_RADIX;
+  const int P = (end_bit - begin_bit + 7) / 8;
+  if (begin_bit != 0 || P < 1 || P > 4) return cudaErrorInvalidValue;
+  uint32_t* ghist = (uint32_t*)tmp;
+  uint32_t* dstart = ghist + 4 * RS_RADIX;
+  uint32_t* tickets = dstart + 4 * RS_RADIX;
+  unsigned long long* status = (unsigned long long*)(tickets + 8);  // 32-byte aligned
+  cudaError_t e = cudaMemsetAsync(tmp, 0, radix_sort_tmp_bytes(n) - 256, st);
+  if (e != cudaSuccess) return e;
+  uint32_t hb = (n + RS_THREADS * 16 - 1) / (RS_THREADS * 16);
+  if (hb > 148 * 8) hb = 148 * 8;
+  k_rs_hist_all<<<hb, RS_THREADS, 0, st>>>(n, keys_a, P, ghist);
+  k_rs_digit_start<<<1, RS_RADIX, 0, st>>>(P, ghist, dstart);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
-  int passes = 0;
-  for (int sh = begin_bit; sh < end_bit; sh += 8) {
-    k_rs_hist<<<G, RS_THREADS, 0, st>>>(n, ki, sh, hist, G);
-    cudaError_t e = exclusive_scan_u32_inplace(G * RS_RADIX, hist, partial, st, launches);
-    if (e != cudaSuccess) return e;
-    k_rs_scatter<<<G, RS_THREADS, 0, st>>>(n, ki, vi, ko, vo, sh, hist, G);
-    if (launches) *launches += 2;
+  for (int p = 0; p < P; ++p) {
+    k_rs_onesweep<<<G, RS_THREADS, 0, st>>>(n, ki, vi, ko, vo, 8 * p, dstart + p * RS_RADIX,
+                                            status + (size_t)p * G * RS_RADIX, tickets + p);
     uint32_t* t;
     t = ki; ki = ko; ko = t;
     t = vi; vi = vo; vo = t;
-    ++passes;
   }
-  if (passes & 1) {  // result must land in (keys_a, vals_a)
+  if (launches) *launches += 2 + P;
+  if (P & 1) {  // result must land in (keys_a, vals_a)
     cudaMemcpyAsync(keys_a, ki, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(vals_a, vi, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
   }
