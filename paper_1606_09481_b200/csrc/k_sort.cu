@@ -10,8 +10,11 @@ namespace rhg {
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;                       // per thread
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // 4096 keys per block
+#ifndef RHG_RS_ITEMS
+#define RHG_RS_ITEMS 16
+#endif
+constexpr int RS_ITEMS = RHG_RS_ITEMS;             // per thread
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;     // keys per tile
 constexpr int RS_RADIX = 256;
 
 // One read of the keys: the digit histograms of all passes (shift 8 p, p < P).
@@ -77,8 +80,9 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
   __shared__ uint32_t tstart[RS_RADIX];
   __shared__ uint32_t gbase[RS_RADIX];
   __shared__ uint32_t wsum[RS_WARPS];
-  __shared__ uint32_t skey[RS_TILE];
-  __shared__ uint32_t sval[RS_TILE];
+  extern __shared__ uint32_t rs_dyn[];  // RS_TILE keys then RS_TILE values
+  uint32_t* skey = rs_dyn;
+  uint32_t* sval = rs_dyn + RS_TILE;
   __shared__ uint32_t tile_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
@@ -349,9 +353,16 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
   k_rs_hist_all<<<hb, RS_THREADS, 0, st>>>(n, keys_a, P, ghist);
   k_rs_digit_start<<<1, RS_RADIX, 0, st>>>(P, ghist, dstart);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
+  constexpr int dyn = 2 * RS_TILE * (int)sizeof(uint32_t);
+  static bool attr = false;  // opt in to > 48 KB of dynamic shared memory once
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   for (int p = 0; p < P; ++p) {
-    k_rs_onesweep<<<G, RS_THREADS, 0, st>>>(n, ki, vi, ko, vo, 8 * p, dstart + p * RS_RADIX,
-                                            status + (size_t)p * G * RS_RADIX, tickets + p);
+    k_rs_onesweep<<<G, RS_THREADS, dyn, st>>>(n, ki, vi, ko, vo, 8 * p, dstart + p * RS_RADIX,
+                                              status + (size_t)p * G * RS_RADIX, tickets + p);
     uint32_t* t;
     t = ki; ki = ko; ko = t;
     t = vi; vi = vo; vo = t;
