@@ -385,6 +385,20 @@ __device__ __forceinline__ void write_edge(const QueryArgs& A, unsigned long lon
   else reinterpret_cast<uint2*>(A.pairs)[o] = vid < w ? make_uint2(vid, w) : make_uint2(w, vid);
 }
 
+// 32 x 32 bit-matrix transpose across the warp: on entry lane r holds row r (bit c =
+// element (r, c)); on exit lane c holds column c (bit r = element (r, c)).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int sft = 16 >> k;
+    const uint32_t m = M[k];
+    const uint32_t o = __shfl_xor_sync(FULL, x, sft);
+    x = (lane & sft) ? ((x & ~m) | ((o >> sft) & m)) : ((x & m) | ((o << sft) & ~m));
+  }
+  return x;
+}
+
 // lanes [lo, hi) of a 32-bit mask (0 <= lo, hi <= 32)
 __device__ __forceinline__ uint32_t lane_range_mask(int lo, int hi) {
   if (hi <= lo) return 0u;
@@ -673,8 +687,10 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     }
   }
   uint32_t deg = 0;           // count pass
-  uint32_t bitpos = 0, word = 0;
-  uint32_t* const wbits = A.bits + (uint64_t)g * (kLightBitRows * 32u) + lane;
+  uint32_t word = 0;
+  // the warp's test bit stream: one ballot word per test iteration, slab after slab
+  uint32_t* const wstream = A.bits + (uint64_t)g * (kLightBitRows * 32u);
+  uint32_t F = 0;             // words of earlier slabs
   bool retest = MODE == QM_EMIT;
   if (MODE == QM_EMIT_BITS) retest = A.warp_over[g] != 0;
   bool over = false;          // count: some lane ran out of bit words
@@ -765,22 +781,17 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     const uint32_t x1 = gbase + (uint32_t)e1, xw = (uint32_t)wx;
     if (MODE == QM_COUNT) tested += nt;
     if (MODE == QM_EMIT_BITS && !retest) {
-      // replay: walk only the set bits of my words covering [bitpos, bitpos + nt)
-      const uint32_t bp0 = bitpos, bp1 = bitpos + nt;
-      const uint32_t wlo = bp0 >> 5, nw = nt ? ((bp1 + 31u) >> 5) - wlo : 0u;
-      const uint32_t mw = __reduce_max_sync(FULL, nw);
-      for (uint32_t u = 0; u < mw; ++u) {
-        uint32_t m = 0;
-        const uint32_t wb = (wlo + u) << 5;  // first bit position of this word
-        if (u < nw) {
-          m = wbits[(wlo + u) * 32u];
-          if (wb < bp0) m &= ~0u << (bp0 - wb);
-          if (bp1 - wb < 32u) m &= (1u << (bp1 - wb)) - 1u;
-        }
+      // replay: word F + i of the warp's bit stream is the ballot of the count pass's
+      // i-th test iteration of this slab (bit l: lane l's i-th candidate).  Per 32
+      // iterations one coalesced load and a 32 x 32 bit transpose give each lane its
+      // own hit mask; then only the set bits are walked.
+      for (uint32_t i0 = 0; i0 < mt; i0 += 32u) {
+        uint32_t m = i0 + (uint32_t)lane < mt ? wstream[F + i0 + (uint32_t)lane] : 0u;
+        m = transpose32(m, lane);
         const uint32_t mh = __reduce_max_sync(FULL, (uint32_t)__popc(m));
         for (uint32_t h = 0; h < mh; ++h) {
           if (m) {
-            const uint32_t i = wb + (uint32_t)(__ffs(m) - 1) - bp0;
+            const uint32_t i = i0 + (uint32_t)(__ffs(m) - 1);
             m &= m - 1u;
             const uint32_t p = pa + i + (i >= thr ? hl : 0u);
             if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
@@ -788,10 +799,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
           }
         }
       }
-      bitpos = bp1;
+      F += mt;
       continue;
     }
     // count, or emit with re-tests: every candidate is tested
+    const bool store = F + mt <= kLightBitRows * 32u;  // warp-uniform
+    if (MODE == QM_COUNT && !store) over = true;
     auto test_loop = [&](auto short_poly) {
       for (uint32_t i = 0; i < mt; ++i) {
         const bool act = i < nt;
@@ -812,13 +825,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
 
         if (MODE == QM_COUNT) {
           deg += hit;
-          word |= (uint32_t)hit << (bitpos & 31u);  // hit is false for idle lanes
-          bitpos += act;
-          if (act && (bitpos & 31u) == 0) {  // a 32-test group completed
-            if ((bitpos >> 5) <= kLightBitRows) wbits[((bitpos >> 5) - 1) * 32u] = word;
-            else over = true;
-            word = 0;
-          }
+          // one ballot word per test iteration; lane (i mod 32) keeps it, and every 32
+          // iterations (or at the slab's last) the lanes store their words at once
+          const uint32_t hm = __ballot_sync(FULL, hit);
+          if ((i & 31u) == (uint32_t)lane) word = hm;
+          if (((i & 31u) == 31u || i + 1 == mt) && store && (uint32_t)lane <= (i & 31u))
+            wstream[F + (i & ~31u) + (uint32_t)lane] = word;
         } else if (hit) {
           if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
           else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
@@ -827,11 +839,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     };
     if (small) test_loop(std::true_type{});
     else test_loop(std::false_type{});
-    if (MODE != QM_COUNT) bitpos += nt;
-    if (MODE == QM_COUNT && nt > 0 && (bitpos & 31u)) {  // partial group: stored now, completed later
-      if ((bitpos >> 5) < kLightBitRows) wbits[(bitpos >> 5) * 32u] = word;
-      else over = true;
-    }
+    F += mt;
   }
   if (MODE == QM_COUNT) {
     if (valid) {
