@@ -603,10 +603,10 @@ __device__ __forceinline__ double inv4s_of(double s) {
 }
 
 #ifndef RHG_QK_MINB_COUNT
-#define RHG_QK_MINB_COUNT 9  // 56 registers, no spills (measured: marginally faster than 64)
+#define RHG_QK_MINB_COUNT 8  // 64 registers (measured at config 3: 2.43 ms vs 2.49 ms with 56)
 #endif
 #ifndef RHG_QK_MINB_EMIT
-#define RHG_QK_MINB_EMIT 9
+#define RHG_QK_MINB_EMIT 8
 #endif
 #ifndef RHG_QK_MINB_SEQ
 #define RHG_QK_MINB_SEQ 7  // 72 registers: the eight sector registers of SecWriter
