@@ -606,7 +606,7 @@ __device__ __forceinline__ double inv4s_of(double s) {
 #define RHG_QK_MINB_COUNT 8  // 64 registers (measured at config 3: 2.43 ms vs 2.49 ms with 56)
 #endif
 #ifndef RHG_QK_MINB_EMIT
-#define RHG_QK_MINB_EMIT 8
+#define RHG_QK_MINB_EMIT 9
 #endif
 #ifndef RHG_QK_MINB_SEQ
 #define RHG_QK_MINB_SEQ 7  // 72 registers: the eight sector registers of SecWriter
