@@ -997,7 +997,13 @@ __global__ void __launch_bounds__(HV_THREADS) k_heavy_chunk_map(const HeavyArgs 
 // + popcount).  Certain pieces count as hits without a test.  Ballot words are
 // stored per chunk (CH / 32 + 8 words per chunk) for the emit pass to replay.
 template <int MODE, int FMT>
-__global__ void __launch_bounds__(HV_THREADS, 4)
+#ifndef RHG_HV_MINB
+#define RHG_HV_MINB 4
+#endif
+#ifndef RHG_HV_BLOCKS
+#define RHG_HV_BLOCKS 8  // per SM
+#endif
+__global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
     k_heavy(const QueryArgs A, const HeavyArgs H, const __grid_constant__ BandConst bc) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
@@ -1122,7 +1128,7 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
 
 cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                          const BandConst& bc, cudaStream_t st) {
-  const uint32_t blocks = 148 * 8;
+  const uint32_t blocks = 148 * RHG_HV_BLOCKS;
   if (mode == QM_COUNT) {
     if (fmt == RHG_CSR) k_heavy<QM_COUNT, RHG_CSR><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);
     else k_heavy<QM_COUNT, RHG_EDGES_UNDIRECTED><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);

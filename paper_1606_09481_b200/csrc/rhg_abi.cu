@@ -127,7 +127,10 @@ struct Layout {
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
-constexpr uint64_t kChunkMin = 1024;
+#ifndef RHG_CHUNK_MIN
+#define RHG_CHUNK_MIN 1024
+#endif
+constexpr uint64_t kChunkMin = RHG_CHUNK_MIN;
 
 int bands_for(uint64_t n, const rhg_options* opt) {
   return (opt && opt->num_bands > 0) ? opt->num_bands : default_bands(n);
