@@ -543,7 +543,7 @@ def test_sorted_vertex_order_host_buffers_and_shards(rhg):
     assert np.array_equal(deg_sum, np.diff(rp))
 
 
-@pytest.mark.parametrize("fmt,order", [("csr", 0), ("pairs", 0), ("csr", 1)])
+@pytest.mark.parametrize("fmt,order", [("csr", 0), ("pairs", 0), ("csr", 1), ("pairs", 1)])
 def test_wide_positions_path_matches(rhg, fmt, order):
     """The 64-bit-position light kernels (taken for n >= 2^30, which does not fit one
     GPU's memory) forced at config 4: identical output to the 32-bit path."""
