@@ -806,35 +806,37 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     const bool store = F + mt <= kLightBitRows * 32u;  // warp-uniform
     if (MODE == QM_COUNT && !store) over = true;
     auto test_loop = [&](auto short_poly) {
-      for (uint32_t i = 0; i < mt; ++i) {
-        const bool act = i < nt;
-        const uint32_t p = pa + i + (i >= thr ? hl : 0u);
-        bool tst = act;
-        if (anyown) tst = tst && !((p - x1) < xw || (p - x1 - nj) < xw);
-        uint32_t r[8];
-        const PointRec* wp = A.pts + (tst ? p : 0u);
-        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                       "=r"(r[6]), "=r"(r[7])
-                     : "l"(wp));
-        const double2 w0 = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
-        const double2 w1 = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
-        const bool hit = decltype(short_poly)::value
-                             ? certified_edge_short(q.theta, q4s, q.a, q.b, w0, w1, T4, tst)
-                             : certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, tst);
-
-        if (MODE == QM_COUNT) {
-          deg += hit;
-          // one ballot word per test iteration; lane (i mod 32) keeps it, and every 32
-          // iterations (or at the slab's last) the lanes store their words at once
-          const uint32_t hm = __ballot_sync(FULL, hit);
-          if ((i & 31u) == (uint32_t)lane) word = hm;
-          if (((i & 31u) == 31u || i + 1 == mt) && store && (uint32_t)lane <= (i & 31u))
-            wstream[F + (i & ~31u) + (uint32_t)lane] = word;
-        } else if (hit) {
-          if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
-          else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
+      // chunks of 32 iterations: lane u keeps the ballot word of iteration i0 + u and
+      // the chunk's words are stored together (count pass)
+      for (uint32_t i0 = 0; i0 < mt; i0 += 32u) {
+        const uint32_t cnt = min(32u, mt - i0);
+        for (uint32_t u = 0; u < cnt; ++u) {
+          const uint32_t i = i0 + u;
+          const bool act = i < nt;
+          const uint32_t p = pa + i + (i >= thr ? hl : 0u);
+          bool tst = act;
+          if (anyown) tst = tst && !((p - x1) < xw || (p - x1 - nj) < xw);
+          uint32_t r[8];
+          const PointRec* wp = A.pts + (tst ? p : 0u);
+          asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                         "=r"(r[6]), "=r"(r[7])
+                       : "l"(wp));
+          const double2 w0 = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+          const double2 w1 = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
+          const bool hit = decltype(short_poly)::value
+                               ? certified_edge_short(q.theta, q4s, q.a, q.b, w0, w1, T4, tst)
+                               : certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, tst);
+          if (MODE == QM_COUNT) {
+            deg += hit;
+            const uint32_t hm = __ballot_sync(FULL, hit);
+            word = u == (uint32_t)lane ? hm : word;
+          } else if (hit) {
+            if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
+            else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
+          }
         }
+        if (MODE == QM_COUNT && store && (uint32_t)lane < cnt) wstream[F + i0 + (uint32_t)lane] = word;
       }
     };
     if (small) test_loop(std::true_type{});
