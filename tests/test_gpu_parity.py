@@ -172,6 +172,10 @@ def test_edge_cases(rhg, orc):
             g = rhg.generate_from_points(*_cpu_pts(th, r), R, fmt)
             k = csr_checked_pairs(g) if fmt == "csr" else pairs_checked(g)
             compare_sets(k, es)
+            # the same with ids in (slab, angle) order, mapped back through perm
+            g1 = rhg.generate_from_points(*_cpu_pts(th, r), R, fmt, options=dict(vertex_order=1))
+            k1 = csr_checked_pairs(g1) if fmt == "csr" else pairs_checked(g1)
+            compare_sets(relabel_keys(k1, g1.perm.cpu().numpy().view(np.uint32).astype(np.int64)), es)
     # complete graph check explicitly
     th, r, R = cases[2]
     g = rhg.generate_from_points(*_cpu_pts(th, r), R, "pairs")
