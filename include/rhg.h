@@ -84,7 +84,11 @@ typedef struct {
   /* 1: run the light query kernels with 64-bit slab positions even when every slab
      holds < 2^30 points (the path n >= 2^30 takes; a test knob, same output). */
   int wide_positions;
-  int reserved[1];
+  /* 1: record the call's kernels as two CUDA graphs (before / after the edge-count
+     readback) and replay them while the arguments (sizes, pointers, seed, options,
+     stream) stay the same; re-captured when they change.  Needs a non-default
+     stream; ignored when timing is requested.  Same output. */
+  int graph;
 } rhg_options;
 
 /* Per-phase device times (CUDA events on the caller's stream), filled when

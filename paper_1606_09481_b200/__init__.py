@@ -46,7 +46,7 @@ class Options(ctypes.Structure):
     _fields_ = [("num_bands", ctypes.c_int), ("band_ratio", ctypes.c_double),
                 ("heavy_threshold", ctypes.c_uint32), ("shard_index", ctypes.c_int),
                 ("shard_count", ctypes.c_int), ("vertex_order", ctypes.c_int),
-                ("wide_positions", ctypes.c_int), ("reserved", ctypes.c_int * 1)]
+                ("wide_positions", ctypes.c_int), ("graph", ctypes.c_int)]
 
 
 class Timing(ctypes.Structure):
@@ -188,7 +188,7 @@ def _options(options) -> Options:
     return Options(int(options.get("num_bands", 0)), float(options.get("band_ratio", 0.0)),
                    int(options.get("heavy_threshold", 0)), int(options.get("shard_index", 0)),
                    int(options.get("shard_count", 0)), int(options.get("vertex_order", 0)),
-                   int(options.get("wide_positions", 0)))
+                   int(options.get("wide_positions", 0)), int(options.get("graph", 0)))
 
 
 def version() -> str:

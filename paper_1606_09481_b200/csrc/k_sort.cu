@@ -335,6 +335,16 @@ size_t radix_sort_tmp_bytes(uint64_t n) {
   return (size_t)(2 * 4 * RS_RADIX + 8) * sizeof(uint32_t) + 4 * G * RS_RADIX * 8ull + 256;
 }
 
+// opt in to > 48 KB of dynamic shared memory once (outside any stream capture)
+cudaError_t radix_sort_prepare() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             2 * RS_TILE * (int)sizeof(uint32_t));
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
 cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
                        uint32_t* vals_b, void* tmp, int begin_bit, int end_bit, cudaStream_t st,
                        int* launches) {
@@ -354,12 +364,8 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
   k_rs_digit_start<<<1, RS_RADIX, 0, st>>>(P, ghist, dstart);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
   constexpr int dyn = 2 * RS_TILE * (int)sizeof(uint32_t);
-  static bool attr = false;  // opt in to > 48 KB of dynamic shared memory once
-  if (!attr) {
-    e = cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  e = radix_sort_prepare();
+  if (e != cudaSuccess) return e;
   for (int p = 0; p < P; ++p) {
     k_rs_onesweep<<<G, RS_THREADS, dyn, st>>>(n, ki, vi, ko, vo, 8 * p, dstart + p * RS_RADIX,
                                               status + (size_t)p * G * RS_RADIX, tickets + p);

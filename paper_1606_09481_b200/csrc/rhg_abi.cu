@@ -5,6 +5,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <vector>
+
 #include "rhg_internal.cuh"
 
 using namespace rhg;
@@ -281,6 +283,43 @@ struct Timer {
   }
 };
 
+// CUDA-graph replay of the two halves of a call (rhg_options.graph): one cached
+// executable per half and thread, re-captured whenever the arguments change.
+struct GraphSlot {
+  std::vector<char> key;
+  cudaGraphExec_t exec = nullptr;
+};
+struct GraphCache {
+  GraphSlot a, b;
+};
+GraphCache& graph_cache() {
+  static thread_local GraphCache gc;
+  return gc;
+}
+template <typename F>
+rhg_status graph_run(GraphSlot& g, const std::vector<char>& key, cudaStream_t st, F&& fn) {
+  if (!g.exec || g.key != key) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.key.clear();
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const rhg_status s = fn();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (s != RHG_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    CK(e);
+    const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ei);
+    g.key = key;
+  }
+  CK(cudaGraphLaunch(g.exec, st));
+  return RHG_OK;
+}
+
 // The full pipeline.  sample == true: Philox points (alpha, seed); else the
 // caller's points (theta_in, r_in).
 rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const double* theta_in,
@@ -346,10 +385,19 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   Timer tm;
   tm.init(out->timing != nullptr, st);
   int launches = 0;
+  float ms_h2d = 0;
+  HeavyMeta* hmeta = (HeavyMeta*)(ws + Lw.h_meta);
+  QueryArgs qa{};
+  HeavyArgs ha{};
+  uint64_t* offs = nullptr;
+  SideStream& ss = side_stream();
+  if (!ss.ok) return RHG_ERR_CUDA;
+  CK(radix_sort_prepare());
+  // part A: sampling through the degree scan, ending with the 8-byte readback
+  auto partA = [&]() -> rhg_status {
   tm.mark();  // 0
   CK(cudaMemsetAsync(hist, 0, 4 * kMaxBands, st));
   CK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), st));
-  float ms_h2d = 0;
   if (sample) {
     CK(launch_sample(n, gen, bc, theta, r, keys_a, vals_a, hist, st));
     ++launches;
@@ -368,7 +416,6 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     CK(launch_keys_from_points(n, th_src, r_src, bc, keys_a, vals_a, hist, sc, st));
     ++launches;
   }
-  HeavyMeta* hmeta = (HeavyMeta*)(ws + Lw.h_meta);
   CK(launch_band_layout(bc, hist, lay, hmeta, st));
   ++launches;
   tm.mark();  // 1
@@ -385,7 +432,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   if (order == 1 && out->perm_out)  // id (sorted position) -> sample / input index
     CK(cudaMemcpyAsync(out->perm_out, vals_a, 4 * n,
                        host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st));
-  QueryArgs qa{};
+  qa = QueryArgs{};
   qa.n = (uint32_t)n;
   qa.labels = (uint32_t)order;
   qa.force_wide = (out->options && out->options->wide_positions == 1) ? 1u : 0u;
@@ -402,7 +449,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.cdeg = (uint32_t*)(ws + Lw.cdeg);
   qa.sc = sc;
   if (bc.nshards > 1) CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of other shards stay empty
-  HeavyArgs ha{};
+  ha = HeavyArgs{};
   ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
   ha.plen = (uint32_t*)(ws + Lw.h_plen);
   ha.poff = (uint32_t*)(ws + Lw.h_poff);
@@ -422,8 +469,6 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   ha.chunk_cap = Lw.chunk_cap;
   ha.chunk_min = kChunkMin;
   // hub path on the side stream, light vertices on the caller's stream
-  SideStream& ss = side_stream();
-  if (!ss.ok) return RHG_ERR_CUDA;
   CK(cudaEventRecord(ss.fork, st));
   CK(cudaStreamWaitEvent(ss.s, ss.fork, 0));
   CK(launch_heavy_plan(f, qa, ha, bc, ws + Lw.heavy_scan_tmp, ss.s, &launches));
@@ -436,16 +481,42 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   ++launches;
   CK(cudaStreamWaitEvent(st, ss.join, 0));
   tm.mark();  // 4
-  uint64_t* offs = (f == RHG_CSR) ? row_ptr_dev : offs_ws;
+  offs = (f == RHG_CSR) ? row_ptr_dev : offs_ws;
   CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
   tm.mark();  // 5
   CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+  return RHG_OK;
+  };
+  // graph mode (rhg_options.graph): both parts are captured once per argument set
+  // and replayed as CUDA graphs; the legacy default stream cannot be captured
+  const bool use_graph = out->options && out->options->graph == 1 && !out->timing && st != nullptr;
+  std::vector<char> key;
+  if (use_graph) {
+    auto add = [&](const void* p, size_t b) {
+      key.insert(key.end(), (const char*)p, (const char*)p + b);
+    };
+    const uint64_t hdr[4] = {n, (uint64_t)sample, seed, (uint64_t)(uintptr_t)st};
+    add(hdr, sizeof(hdr));
+    add(&alpha, 8);
+    add(&R, 8);
+    add(&theta_in, sizeof(theta_in));
+    add(&r_in, sizeof(r_in));
+    rhg_output o = *out;
+    o.num_edges = nullptr; o.R_used = nullptr; o.options = nullptr; o.timing = nullptr;
+    add(&o, sizeof(o));
+    add(out->options, sizeof(rhg_options));
+  }
+  GraphCache& gc = graph_cache();
+  rhg_status s2 = use_graph ? graph_run(gc.a, key, st, partA) : partA();
+  if (s2 != RHG_OK) return s2;
   CK(cudaStreamSynchronize(st));
   const DevScalars hs = *pin;
   if (hs.domain_error) return RHG_ERR_DOMAIN;
   *out->num_edges = hs.total;
   if (out->R_used) *out->R_used = R;
   if (hs.total > out->capacity_edges) return RHG_ERR_CAPACITY;
+  // part B: the emit passes (and host copies), sized by the edge total
+  auto partB = [&]() -> rhg_status {
   qa.offs = offs;
   qa.col = col_dev;
   qa.pairs = pairs_dev;
@@ -487,6 +558,15 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
       CK(cudaMemcpyAsync(out->r_out, r, 8 * n, cudaMemcpyDeviceToHost, st));
   }
   tm.mark();  // 7
+  return RHG_OK;
+  };
+  if (use_graph) {
+    key.insert(key.end(), (const char*)&hs.total, (const char*)&hs.total + sizeof(hs.total));
+    s2 = graph_run(gc.b, key, st, partB);
+  } else {
+    s2 = partB();
+  }
+  if (s2 != RHG_OK) return s2;
   if (host || out->timing) CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   if (out->timing) {

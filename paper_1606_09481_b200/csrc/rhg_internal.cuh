@@ -187,6 +187,7 @@ cudaError_t launch_band_layout(const BandConst& bc, const uint32_t* band_hist, B
 // LSD radix sort of (key, val) pairs, 32-bit keys, stable.  Result lands in
 // (keys_a, vals_a).  tmp must hold radix_sort_tmp_bytes(n).
 size_t radix_sort_tmp_bytes(uint64_t n);
+cudaError_t radix_sort_prepare();
 cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b,
                        uint32_t* vals_b, void* tmp, int begin_bit, int end_bit, cudaStream_t st,
                        int* launches);

@@ -20,6 +20,7 @@ ap.add_argument("--heavy", type=int, default=0)
 ap.add_argument("--bands", type=int, default=0)
 ap.add_argument("--ratio", type=float, default=0.0)
 ap.add_argument("--order", type=int, default=0)
+ap.add_argument("--graph", type=int, default=0)
 a = ap.parse_args()
 n, kbar, gamma, seed, fmt = CFG[a.cfg]
 fmt = a.fmt or fmt

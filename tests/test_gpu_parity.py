@@ -562,3 +562,44 @@ def test_wide_positions_path_matches(rhg, fmt, order):
     else:
         ka, kb = pairs_checked(a), pairs_checked(b)
     assert np.array_equal(ka, kb)
+
+
+def test_graph_mode_replays_identically(rhg):
+    """rhg_options.graph = 1: the call is captured into two CUDA graphs and replayed;
+    repeated calls into the same buffers, a changed seed (re-capture) and both
+    formats give the eager output."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for fmt, cfg in (("csr", 2), ("pairs", 4), ("csr", 4)):
+            n, kbar, gamma, seed = CONFIGS[cfg]
+            ws = rhg.Workspace("cuda")
+            eager = rhg.generate(n, kbar, gamma, seed, fmt, workspace=ws, stream=s)
+            e2 = rhg.generate(n, kbar, gamma, seed + 1, fmt, workspace=ws, stream=s)
+            cap = max(eager.num_edges, e2.num_edges) + 64
+            rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            col = torch.empty(cap, dtype=torch.int32, device="cuda")
+            pr = torch.empty((cap, 2), dtype=torch.int32, device="cuda")
+            bufs = lambda _c: (rp if fmt == "csr" else None, col if fmt == "csr" else None,
+                               pr if fmt != "csr" else None, None, None)
+
+            def run(sd):
+                return rhg._run(lambda o, st: rhg.lib().rhg_generate(n, kbar, gamma, sd, o, st),
+                                n, fmt, kbar, device="cuda", capacity=cap, options=dict(graph=1),
+                                timing=False, workspace=ws, stream=s, host_buffers=False,
+                                want_points=False, sample=True, out_bufs=bufs)
+
+            for rep in range(3):
+                g = run(seed)
+                s.synchronize()
+                assert g.num_edges == eager.num_edges
+                if fmt == "csr":
+                    assert torch.equal(rp, eager.row_ptr) and torch.equal(g.col, eager.col)
+                else:
+                    assert torch.equal(g.pairs, eager.pairs)
+            g2 = run(seed + 1)
+            s.synchronize()
+            assert g2.num_edges == e2.num_edges
+            if fmt == "csr":
+                assert torch.equal(g2.col, e2.col)
+            else:
+                assert torch.equal(g2.pairs, e2.pairs)
