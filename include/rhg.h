@@ -153,8 +153,11 @@ size_t rhg_workspace_bytes(uint64_t n, rhg_format format, uint64_t capacity_edge
    getTargetRadius (line 2), then on `stream`: Philox point sampling (lines 7-8;
    vertex i uses counter i, key = seed, Z12), band assignment (line 9),
    angular sort per band (lines 11-12), range queries with exact tests (lines
-   13-21), and emission into `out`.  Synchronises once on an 8-byte edge count
-   (capacity check).  Deterministic for fixed (n, kbar, gamma, seed, options). */
+   13-21), and emission into `out`.  Device buffers: the emit kernels compare the
+   edge total with capacity_edges on the device (nothing is written if it does not
+   fit) and the call synchronises once, at the end; host buffers: one readback of
+   the 8-byte total sizes the copies.  Deterministic for fixed (n, kbar, gamma, seed,
+   options). */
 rhg_status rhg_generate(uint64_t n, double kbar, double gamma, uint64_t seed,
                         const rhg_output *out, rhg_stream stream);
 

@@ -616,6 +616,9 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
                                               : (SEQ ? RHG_QK_MINB_SEQ : RHG_QK_MINB_EMIT))
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
+  // emit launched before the host has seen the edge total: nothing is written
+  // unless it fits the caller's capacity (block-uniform exit)
+  if (MODE != QM_COUNT && A.total_dev && *A.total_dev > A.cap) return;
   __shared__ BandSm bs;
   __shared__ SlabC scs[kMaxBands];
   __shared__ __align__(16) uint32_t stage_all[(MODE == QM_COUNT || SEQ) ? 4 : QK_THREADS * kStageStride];
@@ -1007,6 +1010,7 @@ template <int MODE, int FMT>
 #endif
 __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
     k_heavy(const QueryArgs A, const HeavyArgs H, const __grid_constant__ BandConst bc) {
+  if (MODE != QM_COUNT && A.total_dev && *A.total_dev > A.cap) return;  // see k_query
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
   const unsigned long long gw = blockIdx.x * HV_WARPS + (threadIdx.x >> 5);

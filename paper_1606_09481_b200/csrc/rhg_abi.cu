@@ -506,21 +506,18 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     add(&o, sizeof(o));
     add(out->options, sizeof(rhg_options));
   }
-  GraphCache& gc = graph_cache();
-  rhg_status s2 = use_graph ? graph_run(gc.a, key, st, partA) : partA();
-  if (s2 != RHG_OK) return s2;
-  CK(cudaStreamSynchronize(st));
-  const DevScalars hs = *pin;
-  if (hs.domain_error) return RHG_ERR_DOMAIN;
-  *out->num_edges = hs.total;
-  if (out->R_used) *out->R_used = R;
-  if (hs.total > out->capacity_edges) return RHG_ERR_CAPACITY;
-  // part B: the emit passes (and host copies), sized by the edge total
+  // part B: the emit passes (and host copies).  Device buffers: enqueued right
+  // behind part A -- the emit kernels read the edge total on the device and write
+  // nothing if it exceeds the capacity -- so the call synchronises once, at the end.
+  // Host buffers: the copies are sized by the total, read back in between.
+  uint64_t copy_total = 0;
   auto partB = [&]() -> rhg_status {
   qa.offs = offs;
   qa.col = col_dev;
   qa.pairs = pairs_dev;
-  qa.out_cap = hs.total;
+  qa.total_dev = &sc->total;
+  qa.cap = out->capacity_edges;
+  qa.out_cap = out->capacity_edges;
   // hub chunks replay their bits unless the hub bit buffer was too small (checked
   // on the device); light warps replay theirs unless they ran out of bit words.
   CK(cudaEventRecord(ss.fork, st));
@@ -547,10 +544,10 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   if (host) {
     if (f == RHG_CSR) {
       CK(cudaMemcpyAsync(out->row_ptr, row_ptr_dev, 8 * (n + 1), cudaMemcpyDeviceToHost, st));
-      if (hs.total)
-        CK(cudaMemcpyAsync(out->col, col_dev, 4 * hs.total, cudaMemcpyDeviceToHost, st));
-    } else if (hs.total) {
-      CK(cudaMemcpyAsync(out->pairs, pairs_dev, 8 * hs.total, cudaMemcpyDeviceToHost, st));
+      if (copy_total)
+        CK(cudaMemcpyAsync(out->col, col_dev, 4 * copy_total, cudaMemcpyDeviceToHost, st));
+    } else if (copy_total) {
+      CK(cudaMemcpyAsync(out->pairs, pairs_dev, 8 * copy_total, cudaMemcpyDeviceToHost, st));
     }
     if (sample && out->theta_out)
       CK(cudaMemcpyAsync(out->theta_out, theta, 8 * n, cudaMemcpyDeviceToHost, st));
@@ -560,11 +557,38 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   tm.mark();  // 7
   return RHG_OK;
   };
-  if (use_graph) {
-    key.insert(key.end(), (const char*)&hs.total, (const char*)&hs.total + sizeof(hs.total));
-    s2 = graph_run(gc.b, key, st, partB);
+  GraphCache& gc = graph_cache();
+  rhg_status s2 = RHG_OK;
+  DevScalars hs;
+  if (!host) {
+    auto both = [&]() -> rhg_status {
+      const rhg_status sa = partA();
+      return sa != RHG_OK ? sa : partB();
+    };
+    s2 = use_graph ? graph_run(gc.a, key, st, both) : both();
+    if (s2 != RHG_OK) return s2;
+    CK(cudaStreamSynchronize(st));
+    hs = *pin;
+    if (hs.domain_error) return RHG_ERR_DOMAIN;
+    *out->num_edges = hs.total;
+    if (out->R_used) *out->R_used = R;
+    if (hs.total > out->capacity_edges) return RHG_ERR_CAPACITY;  // the emit wrote nothing
   } else {
-    s2 = partB();
+    s2 = use_graph ? graph_run(gc.a, key, st, partA) : partA();
+    if (s2 != RHG_OK) return s2;
+    CK(cudaStreamSynchronize(st));
+    hs = *pin;
+    if (hs.domain_error) return RHG_ERR_DOMAIN;
+    *out->num_edges = hs.total;
+    if (out->R_used) *out->R_used = R;
+    if (hs.total > out->capacity_edges) return RHG_ERR_CAPACITY;
+    copy_total = hs.total;
+    if (use_graph) {
+      key.insert(key.end(), (const char*)&hs.total, (const char*)&hs.total + sizeof(hs.total));
+      s2 = graph_run(gc.b, key, st, partB);
+    } else {
+      s2 = partB();
+    }
   }
   if (s2 != RHG_OK) return s2;
   if (host || out->timing) CK(cudaStreamSynchronize(st));

@@ -126,6 +126,8 @@ struct QueryArgs {
   DevScalars* sc;
   uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
   uint32_t force_wide;                // 64-bit slab positions in the light kernels
+  const unsigned long long* total_dev;  // emit: skip everything if *total_dev > cap
+  unsigned long long cap;
 };
 
 // Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.

@@ -239,6 +239,21 @@ def test_capacity_protocol(rhg):
     g = rhg.generate(n, kbar, gamma, seed, "csr")
     g2 = rhg.generate(n, kbar, gamma, seed, "csr", capacity=g.num_edges)
     assert torch.equal(g.col, g2.col)
+    # device buffers: the emit runs behind the count without a host readback and must
+    # write nothing when the total does not fit
+    for fmt in ("csr", "pairs"):
+        cap = 1000
+        col = torch.full((cap,), -1, dtype=torch.int32, device="cuda")
+        pr = torch.full((cap, 2), -1, dtype=torch.int32, device="cuda")
+        rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        with pytest.raises(rhg.RhgError) as ei:
+            rhg._run(lambda o, st: rhg.lib().rhg_generate(n, kbar, gamma, seed, o, st), n, fmt, kbar,
+                     device="cuda", capacity=cap, options=None, timing=False, workspace=None,
+                     stream=None, host_buffers=False, want_points=False, sample=True,
+                     out_bufs=lambda _c: (rp, col, pr, None, None))
+        assert ei.value.status == rhg.RHG_ERR_CAPACITY
+        torch.cuda.synchronize()
+        assert bool((col == -1).all()) and bool((pr == -1).all()), "edges written past capacity"
 
 
 def test_host_buffers_mode(rhg, orc):
