@@ -105,11 +105,12 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     const bool valid = i < n;
     const uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = wcnt[w][d & 0xFFu];
-    loc[it] = before + __popc(peers & lt);
-    __syncwarp();
-    if (valid && (__ffs(peers) - 1) == lane) wcnt[w][d] = before + __popc(peers);
-    __syncwarp();
+    // the group leader reserves the group's slots with one shared-memory atomic
+    // (same-address atomics of one warp execute in issue order: stable)
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && leader == lane) old = atomicAdd(&wcnt[w][d], (uint32_t)__popc(peers));
+    loc[it] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
   }
   __syncthreads();
   // per digit: exclusive prefix over warps (warp order = item order => stable),
