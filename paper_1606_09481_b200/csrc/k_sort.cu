@@ -127,15 +127,30 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     }
     volatile unsigned long long* my = status + (size_t)tile * RS_RADIX + d;
     *my = (tile == 0 ? kRsIncl : kRsAgg) | run;
+    // look back over up to kLb earlier tiles per round (their words loaded together),
+    // summing tile counts until an inclusive prefix
+#ifndef RHG_RS_LOOKBACK
+#define RHG_RS_LOOKBACK 4
+#endif
+    constexpr uint32_t kLb = RHG_RS_LOOKBACK;
     unsigned long long excl = 0;
-    for (uint32_t t2 = tile; t2 > 0; --t2) {
-      const volatile unsigned long long* o = status + (size_t)(t2 - 1) * RS_RADIX + d;
-      unsigned long long v;
-      do {
-        v = *o;
-      } while ((v & ~kRsVal) == 0ull);
-      excl += v & kRsVal;
-      if ((v & ~kRsVal) == kRsIncl) break;
+    for (uint32_t t2 = tile; t2 > 0;) {
+      const uint32_t k = t2 < kLb ? t2 : kLb;
+      unsigned long long v[kLb];
+#pragma unroll
+      for (uint32_t j = 0; j < kLb; ++j)
+        v[j] = j < k ? *(const volatile unsigned long long*)(status + (size_t)(t2 - 1 - j) * RS_RADIX + d) : 0ull;
+      bool done = false;
+#pragma unroll
+      for (uint32_t j = 0; j < kLb; ++j) {
+        if (done || j >= k) continue;
+        const volatile unsigned long long* o = status + (size_t)(t2 - 1 - j) * RS_RADIX + d;
+        while ((v[j] & ~kRsVal) == 0ull) v[j] = *o;
+        excl += v[j] & kRsVal;
+        done = (v[j] & ~kRsVal) == kRsIncl;
+      }
+      if (done) break;
+      t2 -= k;
     }
     if (tile) *my = kRsIncl | (excl + run);
     uint32_t inc = run;
