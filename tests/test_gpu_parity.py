@@ -290,7 +290,12 @@ def test_full_size_csr_sampled_rows(rhg, orc, cfg):
     over all 1e7 points, plus symmetry of those rows."""
     n, kbar, gamma, seed = CONFIGS[cfg]
     th_o, r_o, R, a = oracle_points(orc, n, kbar, gamma, seed)
-    g = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True)
+    # as bench.py runs it: CUDA-graph mode on a dedicated stream
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = rhg.generate(n, kbar, gamma, seed, "csr", return_points=True, stream=s,
+                         options=dict(graph=1))
+    s.synchronize()
     assert g.R == pytest.approx(R, rel=1e-13)
     th, r = g.theta.cpu().numpy(), g.r.cpu().numpy()
     assert np.array_equal(th, th_o)
