@@ -22,6 +22,20 @@ __device__ __forceinline__ uint32_t warp_incl_u32(uint32_t v) {
 // Doubled SoA: the record of sorted position k in slab j (start s_j, n_j points)
 // is written at k + s_j and k + s_j + n_j, so slab j occupies [2 s_j, 2 s_j + 2 n_j)
 // as two back-to-back copies and every arc across 2 pi is one index range.
+// The query record of one point: e^{r/2} from exp, e^{-r/2} as its correctly
+// rounded reciprocal, and sinh r = (e^{r/2} - e^{-r/2})(e^{r/2} + e^{-r/2}) / 2 for
+// r >= 1 (no cancellation there: the first factor is >= 2 sinh(1/2)), sinh() below.
+// A few ulp from libm's values at most -- far inside the near-tie window the edge
+// predicate is checked against; both endpoints of a pair read the same record.
+__device__ __forceinline__ PointRec point_rec(double th, double rr) {
+  PointRec p;
+  p.theta = th;
+  p.a = exp(0.5 * rr);
+  p.b = __drcp_rn(p.a);
+  p.s = rr >= 1.0 ? 0.5 * ((p.a - p.b) * (p.a + p.b)) : sinh(rr);
+  return p;
+}
+
 __device__ __forceinline__ void put_doubled(uint32_t k, uint32_t key, const BandLayout* lay,
                                             const PointRec& p, uint32_t id,
                                             PointRec* __restrict__ pts, uint32_t* __restrict__ sid2) {
@@ -40,13 +54,7 @@ __global__ void __launch_bounds__(256)
              uint32_t* __restrict__ sid2, int seq_ids) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t i = sidx[k];
-    const double rr = r[i];
-    PointRec p;
-    p.theta = theta[i];
-    p.s = sinh(rr);
-    p.a = exp(0.5 * rr);
-    p.b = exp(-0.5 * rr);
-    put_doubled(k, skey[k], lay, p, seq_ids ? k : i, pts, sid2);
+    put_doubled(k, skey[k], lay, point_rec(theta[i], r[i]), seq_ids ? k : i, pts, sid2);
   }
 }
 
@@ -61,12 +69,7 @@ __global__ void __launch_bounds__(256)
     const uint32_t i = sidx[k];
     double th, rr;
     words_to_point(vertex_words(seed, i), two_over_alpha, half_span, R, th, rr);
-    PointRec p;
-    p.theta = th;
-    p.s = sinh(rr);
-    p.a = exp(0.5 * rr);
-    p.b = exp(-0.5 * rr);
-    put_doubled(k, skey[k], lay, p, seq_ids ? k : i, pts, sid2);
+    put_doubled(k, skey[k], lay, point_rec(th, rr), seq_ids ? k : i, pts, sid2);
   }
 }
 
