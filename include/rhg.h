@@ -40,10 +40,10 @@ typedef enum {
                               Eq. 22 */
   RHG_ERR_WORKSPACE = 4,   /* workspace smaller than rhg_workspace_bytes() asks for */
   RHG_ERR_CAPACITY = 5,    /* output capacity too small; *num_edges holds the required count and
-                              the edge buffers are untouched.  Output is deterministic, so the
-                              caller may reallocate and call again. */
+                              col / pairs are untouched (CSR row_ptr holds the offsets).  Output
+                              is deterministic, so the caller may reallocate and call again. */
   RHG_ERR_DOMAIN = 6,      /* an input point has r outside [0, R] or theta outside [0, 2pi)
-                              (SPEC.md:199), detected on the device */
+                              (SPEC.md:199), detected on the device; output buffers unspecified */
   RHG_ERR_CUDA = 7         /* a CUDA launch or runtime call failed */
 } rhg_status;
 
