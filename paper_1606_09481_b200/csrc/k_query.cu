@@ -61,7 +61,10 @@ namespace rhg {
   } while (0)
 #endif
 
-constexpr int QK_WARPS = 4;
+#ifndef RHG_QK_WARPS
+#define RHG_QK_WARPS 4
+#endif
+constexpr int QK_WARPS = RHG_QK_WARPS;
 constexpr int QK_THREADS = QK_WARPS * 32;
 constexpr uint32_t FULL = 0xffffffffu;
 
