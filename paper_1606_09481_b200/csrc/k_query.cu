@@ -726,12 +726,6 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
         w.dq = w32.dq;
       }
     }
-    // every candidate of the warp within |dphi| < 2^-4 (300000 quanta < 2^27 2^-4 / 2pi)
-    // and no window reaching across theta = 0 (so no seam pair): the short-polynomial
-    // test applies
-    const int32_t q32 = (int32_t)(qkey & kQMask);
-    const bool small = __all_sync(
-        FULL, !on || (!WIDE && w.dq < 300000 && q32 >= w.dq && q32 + w.dq < (int32_t)(1u << kQBits)));
     const bool own = on && (j == (int)qband);
     const bool anyown = __any_sync(FULL, own);
     I e1 = 0, wx = 0;
@@ -845,6 +839,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
         if (MODE == QM_COUNT && store && (uint32_t)lane < cnt) wstream[F + i0 + (uint32_t)lane] = word;
       }
     };
+    // every candidate of the warp within |dphi| < 2^-4 (300000 quanta < 2^27 2^-4 / 2pi)
+    // and no window reaching across theta = 0 (so no seam pair): the short-polynomial
+    // test applies
+    const int32_t q32 = (int32_t)(qkey & kQMask);
+    const bool small = __all_sync(
+        FULL, !on || (!WIDE && w.dq < 300000 && q32 >= w.dq && q32 + w.dq < (int32_t)(1u << kQBits)));
     if (small) test_loop(std::true_type{});
     else test_loop(std::false_type{});
     F += mt;
