@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   bool retest = MODE == QM_EMIT;
   if (MODE == QM_EMIT_BITS) retest = A.warp_over[g] != 0;
   bool over = false;          // count: some lane ran out of bit words
-  unsigned long long tested = 0, certain = 0;
+  uint32_t tested = 0, certain = 0;  // per lane (certain: also the row-tail start)
 
   int jlo = 0;
   if (outward) jlo = (int)__reduce_min_sync(FULL, valid ? qband : 0xffffu);
@@ -860,11 +860,13 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
       A.warp_over[g] = anyover ? 1u : 0u;
       if (anyover) atomicOr(&A.sc->bit_overflow, 1u);
     }
-    tested = warp_incl(tested);
-    certain = warp_incl(certain);
-    if (lane == 31) {
-      atomicAdd(&A.sc->candidates, tested);
-      atomicAdd(&A.sc->certain, certain);
+    if (A.stats) {  // timing statistics only
+      const unsigned long long tw = warp_incl((unsigned long long)tested);
+      const unsigned long long cw = warp_incl((unsigned long long)certain);
+      if (lane == 31) {
+        atomicAdd(&A.sc->candidates, tw);
+        atomicAdd(&A.sc->certain, cw);
+      }
     }
   } else if (valid) {
     if (SEQ) sw.finish(A);

@@ -436,6 +436,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.n = (uint32_t)n;
   qa.labels = (uint32_t)order;
   qa.force_wide = (out->options && out->options->wide_positions == 1) ? 1u : 0u;
+  qa.stats = out->timing ? 1u : 0u;
   qa.pts = pts;
   qa.skey = keys_a;
   qa.sid = vals_a;

@@ -126,6 +126,7 @@ struct QueryArgs {
   DevScalars* sc;
   uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
   uint32_t force_wide;                // 64-bit slab positions in the light kernels
+  uint32_t stats;                     // accumulate candidate / certain totals (timing)
   const unsigned long long* total_dev;  // emit: skip everything if *total_dev > cap
   unsigned long long cap;
 };
