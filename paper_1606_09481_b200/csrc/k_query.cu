@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
           // no tests
           m = __ballot_sync(FULL, act);
           if (MODE == QM_COUNT && bits && lane == 0) H.bits[wbase + bt] = m;
-          if (MODE == QM_COUNT) cert_total += __popc(m);
+          if (MODE == QM_COUNT && A.stats) cert_total += __popc(m);
         } else {
           const bool test = act && !o_cert;
           const double2* xp = reinterpret_cast<const double2*>(A.pts + (test ? p : 0u));
@@ -1091,7 +1091,7 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
           const bool e = certified_edge(q.theta, q4s, q.a, q.b, w0, w1, T4, test);
           m = __ballot_sync(FULL, e || (act && o_cert));
           if (MODE == QM_COUNT && bits && lane == 0) H.bits[wbase + bt] = m;
-          if (MODE == QM_COUNT) {
+          if (MODE == QM_COUNT && A.stats) {
             const uint32_t na = __popc(__ballot_sync(FULL, act));
             const uint32_t nc = __popc(__ballot_sync(FULL, act && o_cert));
             cand_total += na - nc;
