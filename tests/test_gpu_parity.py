@@ -623,3 +623,24 @@ def test_graph_mode_replays_identically(rhg):
                 assert torch.equal(g2.col, e2.col)
             else:
                 assert torch.equal(g2.pairs, e2.pairs)
+
+
+def test_graph_mode_host_buffers(rhg):
+    """Graph mode with host buffers: the emit half is captured per edge total and the
+    copies replayed; output equals the eager device-buffer call."""
+    n, kbar, gamma, seed = CONFIGS[2]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ws = rhg.Workspace("cuda")
+        ref = rhg.generate(n, kbar, gamma, seed, "csr", workspace=ws, stream=s)
+        cap = ref.num_edges
+        rp = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        col = torch.empty(cap, dtype=torch.int32, pin_memory=True)
+        for _ in range(3):
+            g = rhg._run(lambda o, st: rhg.lib().rhg_generate(n, kbar, gamma, seed, o, st), n, "csr",
+                         kbar, device="cuda", capacity=cap, options=dict(graph=1), timing=False,
+                         workspace=ws, stream=s, host_buffers=True, want_points=False, sample=True,
+                         out_bufs=lambda _c: (rp, col, None, None, None))
+            s.synchronize()
+            assert g.num_edges == ref.num_edges
+            assert torch.equal(rp, ref.row_ptr.cpu()) and torch.equal(col, ref.col.cpu())
