@@ -86,22 +86,32 @@ __global__ void __launch_bounds__(256)
   // of a band also owns (bucket(k), nb_j] (value k + 1, written by its lane).
   __shared__ uint8_t tbl[8][32];
   __shared__ uint2 own[8][32];
+  __shared__ uint32_t s_start[kMaxBands + 1], s_off[kMaxBands], s_sh[kMaxBands], s_nb[kMaxBands];
+  if (threadIdx.x <= (unsigned)L) s_start[threadIdx.x] = lay->start[threadIdx.x];
+  if (threadIdx.x < (unsigned)L) {
+    s_off[threadIdx.x] = lay->dir_off[threadIdx.x];
+    s_sh[threadIdx.x] = lay->shift[threadIdx.x];
+    s_nb[threadIdx.x] = lay->nb[threadIdx.x];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + wi; (uint64_t)w * 32 < n; w += nwarps) {
     const uint32_t k = w * 32 + (uint32_t)lane;
     uint32_t len = 0, base = 0, j = 0, b = 0;
+    const uint32_t key = k < n ? __ldg(skey + k) : 0u;
+    uint32_t pkey = __shfl_up_sync(0xffffffffu, key, 1);  // the previous point's key
+    if (lane == 0 && k > 0 && k < n) pkey = __ldg(skey + k - 1);
     if (k < n) {
-      const uint32_t key = __ldg(skey + k);
       j = key >> kBandShift;
-      const uint32_t sh = lay->shift[j], off = lay->dir_off[j];
+      const uint32_t sh = s_sh[j], off = s_off[j];
       b = (key & kQMask) >> sh;
       uint32_t first = 0;  // first entry I own
-      if (k > lay->start[j]) first = ((__ldg(skey + k - 1) & kQMask) >> sh) + 1;
+      if (k > s_start[j]) first = ((pkey & kQMask) >> sh) + 1;
       len = b + 1 - first;  // 0 if the previous point shares my bucket
       base = off + first;
-      if (k + 1 == lay->start[j + 1]) {  // band tail: (b, nb] -> k + 1
-        const uint32_t nb = lay->nb[j];
+      if (k + 1 == s_start[j + 1]) {  // band tail: (b, nb] -> k + 1
+        const uint32_t nb = s_nb[j];
         for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
       }
     }
