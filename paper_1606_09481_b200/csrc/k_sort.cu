@@ -55,10 +55,13 @@ __global__ void __launch_bounds__(RS_RADIX) k_rs_digit_start(int P, const uint32
 }
 
 #ifndef RHG_RS_MINB
-#define RHG_RS_MINB 3
+#define RHG_RS_MINB 4
 #endif
 // Look-back status of (tile, digit): bits 62-63 flag (0 not yet, 1 tile count,
 // 2 inclusive prefix over tiles), bits 0-61 the value.
+#ifndef RHG_RS_BALLOT_MATCH
+#define RHG_RS_BALLOT_MATCH 1
+#endif
 constexpr unsigned long long kRsAgg = 1ull << 62, kRsIncl = 2ull << 62;
 constexpr unsigned long long kRsVal = (1ull << 62) - 1ull;
 
@@ -91,7 +94,8 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
   const uint32_t tile = tile_s;
   const uint32_t tbase = tile * RS_TILE;
   const uint32_t wbase = tbase + w * (32 * RS_ITEMS);
-  uint32_t key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
+  static_assert(RS_ITEMS % 2 == 0 && 32 * RS_ITEMS <= 65536, "two 16-bit ranks per register");
+  uint32_t key[RS_ITEMS], val[RS_ITEMS], loc2[RS_ITEMS / 2];  // rank in the warp's digit run
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {  // all loads in flight before the ranking chain
@@ -104,13 +108,26 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     const uint32_t i = wbase + it * 32 + lane;
     const bool valid = i < n;
     const uint32_t d = valid ? ((key[it] >> shift) & 0xFFu) : (RS_RADIX + lane);
+#if RHG_RS_BALLOT_MATCH
+    // equal-digit peers from 8 bit ballots (+ validity), instead of match.any
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    if (!valid) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+#else
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#endif
     // the group leader reserves the group's slots with one shared-memory atomic
     // (same-address atomics of one warp execute in issue order: stable)
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (valid && leader == lane) old = atomicAdd(&wcnt[w][d], (uint32_t)__popc(peers));
-    loc[it] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+    const uint32_t rk = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
+    if (it & 1) loc2[it >> 1] |= rk << 16; else loc2[it >> 1] = rk;
   }
   __syncthreads();
   // per digit: exclusive prefix over warps (warp order = item order => stable),
@@ -173,7 +190,7 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     const uint32_t i = wbase + it * 32 + lane;
     if (i < n) {
       const uint32_t d = (key[it] >> shift) & 0xFFu;
-      const uint32_t lp = tstart[d] + wcnt[w][d] + loc[it];
+      const uint32_t lp = tstart[d] + wcnt[w][d] + ((loc2[it >> 1] >> (16 * (it & 1))) & 0xFFFFu);
       skey[lp] = key[it];
       sval[lp] = val[it];
     }
