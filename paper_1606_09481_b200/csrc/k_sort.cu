@@ -67,8 +67,9 @@ constexpr unsigned long long kRsVal = (1ull << 62) - 1ull;
 
 // One LSD pass ("onesweep"): tiles take tickets in the order they start; each
 // ranks its keys by digit (warp w of the tile owns items [w*512, +512) and walks
-// them in 16 rounds of 32; __match_any_sync ranks equal digits within a round, so
-// the order is stable), publishes its per-digit counts, and finds the count of
+// them in 16 rounds of 32; 8 bit ballots find the lanes of equal digit in a round,
+// whose leader reserves their slots with one shared-memory atomic, so the order is
+// stable), publishes its per-digit counts, and finds the count of
 // every digit in all earlier tiles by decoupled look-back (thread d walks back over
 // the tiles' (tile, d) words until an inclusive prefix).  The tile is then
 // re-ordered by digit in shared memory and written out so that consecutive threads
