@@ -516,6 +516,43 @@ def test_sorted_vertex_order_matches_oracle(rhg, orc, cfg, fmt):
     assert np.all(dth > -2.0 * 2.0 * np.pi / 2**27), "angle order violated within a slab"
 
 
+def _expected_perm(rhg, th, r, R):
+    """rhg.h vertex_order = 1: slab (c_j <= r < c_{j+1}, last slab closed), then the
+    27-bit angular key trunc(fl(theta * 2^27 / 2pi)) (clamped), ties by input index.
+    The key is taken in fp64 with one rounded multiply, as the library takes it."""
+    c = rhg.band_boundaries(len(th), R)
+    band = np.clip(np.searchsorted(c, r, side="right") - 1, 0, len(c) - 2).astype(np.int64)
+    q = np.minimum(np.floor(th * float.fromhex("0x1.45f306dc9c883p+24")), 2**27 - 1).astype(np.int64)
+    return np.lexsort((np.arange(len(th)), q, band))
+
+
+@pytest.mark.parametrize("case", ["uniform_1e6", "ties", "ragged", "philox"])
+def test_sorted_vertex_order_is_the_stable_key_sort(rhg, orc, case):
+    """perm (vertex_order = 1) equals the stable sort by (slab, angular key) exactly:
+    checks the radix sort's order, its stability on equal keys (many duplicate
+    angles) and partial tiles, index for index."""
+    rng = np.random.default_rng(23)
+    if case == "uniform_1e6":
+        n, kbar, gamma, seed = CONFIGS[2]
+        th, r, R, _ = oracle_points(orc, n, kbar, gamma, seed)
+    elif case == "ties":
+        n, R = 60_000, 24.0
+        th = rng.integers(0, 4096, n) * (2.0 * np.pi / 4096)  # ~15 points per key
+        r = orc.sample_points(n, 1.0, R, 8)[1]
+    elif case == "ragged":
+        n, R = 4096 * 5 + 1234, 22.0
+        th, r = orc.sample_points(n, 0.9, R, 9)
+    if case == "philox":  # generate path: Philox points, re-derived in the gather
+        n, kbar, gamma, seed = CONFIGS[2]
+        g = rhg.generate(n, kbar, gamma, seed, "pairs", options=dict(vertex_order=1),
+                         return_points=True)
+        th, r, R = g.theta.cpu().numpy(), g.r.cpu().numpy(), g.R
+    else:
+        g = rhg.generate_from_points(*_cpu_pts(th, r), R, "pairs", options=dict(vertex_order=1))
+    perm = g.perm.cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(perm, _expected_perm(rhg, th, r, R))
+
+
 def test_sorted_vertex_order_full_size_equals_default(rhg):
     """Config 3 (n = 1e7, kbar = 100): the vertex_order = 1 graph relabelled through
     perm is the default graph, edge for edge (compared on the GPU)."""
