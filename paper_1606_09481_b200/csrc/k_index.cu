@@ -47,104 +47,123 @@ __device__ __forceinline__ void put_doubled(uint32_t k, uint32_t key, const Band
   sid2[k + s + nj] = id;
 }
 
-__global__ void __launch_bounds__(256)
-    k_gather(uint32_t n, const double* __restrict__ theta, const double* __restrict__ r,
-             const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
-             const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
-             uint32_t* __restrict__ sid2, int seq_ids) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const uint32_t i = sidx[k];
-    put_doubled(k, skey[k], lay, point_rec(theta[i], r[i]), seq_ids ? k : i, pts, sid2);
-  }
-}
-
-// Generate path: the points are re-derived from Philox(seed, i) (bit-identical to
-// K1, same device code) instead of gathering theta[i], r[i] at random addresses.
-__global__ void __launch_bounds__(256)
-    k_gather_philox(uint32_t n, uint64_t seed, double two_over_alpha, double half_span, double R,
-                    const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sidx,
-                    const BandLayout* __restrict__ lay, PointRec* __restrict__ pts,
-                    uint32_t* __restrict__ sid2, int seq_ids) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const uint32_t i = sidx[k];
-    double th, rr;
-    words_to_point(vertex_words(seed, i), two_over_alpha, half_span, R, th, rr);
-    put_doubled(k, skey[k], lay, point_rec(th, rr), seq_ids ? k : i, pts, sid2);
-  }
-}
-
+// ---- bucket directory ----
 // dir[dir_off[j] + b] = first sorted position of band j whose bucket >= b, for
-// b = 0 .. nb_j (entry nb_j = band end).  Thread k fills the entries in
-// (bucket(k-1), bucket(k)]; the last point of a band also fills the tail.
-// (Radix-sorted path; the sampled path gets the directory from bucket_sort.)
-__global__ void __launch_bounds__(256)
-    k_directory(uint32_t n, const uint32_t* __restrict__ skey, const BandLayout* __restrict__ lay,
-                int L, uint32_t* __restrict__ dir) {
-  // Warp-cooperative: the entries owned by 32 consecutive points are one contiguous
-  // stretch of the directory (per band), written 32 consecutive entries per store
-  // instruction.  Point k owns (bucket(k-1), bucket(k)] (value k); the last point
-  // of a band also owns (bucket(k), nb_j] (value k + 1, written by its lane).
-  __shared__ uint8_t tbl[8][32];
-  __shared__ uint2 own[8][32];
-  __shared__ uint32_t s_start[kMaxBands + 1], s_off[kMaxBands], s_sh[kMaxBands], s_nb[kMaxBands];
-  if (threadIdx.x <= (unsigned)L) s_start[threadIdx.x] = lay->start[threadIdx.x];
+// b = 0 .. nb_j (entry nb_j = band end).  Point k owns the entries in
+// (bucket(k-1), bucket(k)] (value k); the last point of a band also owns
+// (bucket(k), nb_j] (value k + 1, written by its lane).  Warp-cooperative: the
+// entries owned by 32 consecutive points are one contiguous stretch of the
+// directory (per band), written 32 consecutive entries per store instruction.
+// Runs inside the gather kernels (same warp -> 32 positions mapping, the key is
+// already in a register; the directory's integer work overlaps the gather's
+// memory traffic).  (The sampled path gets its directory from bucket_sort.)
+struct DirSmem {
+  uint8_t tbl[8][32];
+  uint2 own[8][32];
+  uint32_t start[kMaxBands + 1], off[kMaxBands], sh[kMaxBands], nb[kMaxBands];
+};
+
+__device__ __forceinline__ void dir_smem_init(DirSmem& S, const BandLayout* lay, int L) {
+  if (threadIdx.x <= (unsigned)L) S.start[threadIdx.x] = lay->start[threadIdx.x];
   if (threadIdx.x < (unsigned)L) {
-    s_off[threadIdx.x] = lay->dir_off[threadIdx.x];
-    s_sh[threadIdx.x] = lay->shift[threadIdx.x];
-    s_nb[threadIdx.x] = lay->nb[threadIdx.x];
+    S.off[threadIdx.x] = lay->dir_off[threadIdx.x];
+    S.sh[threadIdx.x] = lay->shift[threadIdx.x];
+    S.nb[threadIdx.x] = lay->nb[threadIdx.x];
   }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + wi; (uint64_t)w * 32 < n; w += nwarps) {
-    const uint32_t k = w * 32 + (uint32_t)lane;
-    uint32_t len = 0, base = 0, j = 0, b = 0;
-    const uint32_t key = k < n ? __ldg(skey + k) : 0u;
-    uint32_t pkey = __shfl_up_sync(0xffffffffu, key, 1);  // the previous point's key
-    if (lane == 0 && k > 0 && k < n) pkey = __ldg(skey + k - 1);
-    if (k < n) {
-      j = key >> kBandShift;
-      const uint32_t sh = s_sh[j], off = s_off[j];
-      b = (key & kQMask) >> sh;
-      uint32_t first = 0;  // first entry I own
-      if (k > s_start[j]) first = ((pkey & kQMask) >> sh) + 1;
-      len = b + 1 - first;  // 0 if the previous point shares my bucket
-      base = off + first;
-      if (k + 1 == s_start[j + 1]) {  // band tail: (b, nb] -> k + 1
-        const uint32_t nb = s_nb[j];
-        for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
-      }
+}
+
+// the directory entries owned by positions [32 w, 32 w + 32); key = skey[k] (0 if k >= n)
+__device__ __forceinline__ void dir_warp(uint32_t w, uint32_t n, const uint32_t* __restrict__ skey,
+                                         uint32_t key, DirSmem& S, uint32_t* __restrict__ dir) {
+  const int lane = threadIdx.x & 31, wi = (threadIdx.x >> 5) & 7;
+  const uint32_t k = w * 32 + (uint32_t)lane;
+  uint32_t len = 0, base = 0;
+  uint32_t pkey = __shfl_up_sync(0xffffffffu, key, 1);  // the previous point's key
+  if (lane == 0 && k > 0 && k < n) pkey = __ldg(skey + k - 1);
+  if (k < n) {
+    const uint32_t j = key >> kBandShift;
+    const uint32_t sh = S.sh[j], off = S.off[j];
+    const uint32_t b = (key & kQMask) >> sh;
+    uint32_t first = 0;  // first entry I own
+    if (k > S.start[j]) first = ((pkey & kQMask) >> sh) + 1;
+    len = b + 1 - first;  // 0 if the previous point shares my bucket
+    base = off + first;
+    if (k + 1 == S.start[j + 1]) {  // band tail: (b, nb] -> k + 1
+      const uint32_t nb = S.nb[j];
+      for (uint32_t bb = b + 1; bb <= nb; ++bb) dir[off + bb] = k + 1;
     }
-    const uint32_t incl = warp_incl_u32(len), T = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t pre = incl - len;
-    const uint32_t NE = __ballot_sync(0xffffffffu, len > 0);
-    if (len > 0) {
-      tbl[wi][__popc(NE & ((1u << lane) - 1u))] = (uint8_t)lane;
-      own[wi][lane] = make_uint2(base - pre, k);  // entry t -> dir[base - pre + t] = k
-    }
-    __syncwarp();
-    uint32_t R0 = 0;
-    for (uint32_t B = 0; B < T; B += 32) {
-      const uint32_t sb = pre - B;
-      const uint32_t M = __reduce_or_sync(0xffffffffu, (len > 0 && sb < 32u) ? (1u << sb) : 0u);
-      const uint32_t rank = R0 + __popc(M & (0xffffffffu >> (31 - lane)));
-      R0 += __popc(M);
-      const uint32_t t = B + (uint32_t)lane;
-      if (t < T) {
-        const uint2 o = own[wi][tbl[wi][(rank - 1u) & 31u]];
-        dir[o.x + t] = o.y;
-      }
-    }
-    __syncwarp();
   }
-  // empty bands: both entries = band start
+  const uint32_t incl = warp_incl_u32(len), T = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t pre = incl - len;
+  const uint32_t NE = __ballot_sync(0xffffffffu, len > 0);
+  if (len > 0) {
+    S.tbl[wi][__popc(NE & ((1u << lane) - 1u))] = (uint8_t)lane;
+    S.own[wi][lane] = make_uint2(base - pre, k);  // entry t -> dir[base - pre + t] = k
+  }
+  __syncwarp();
+  uint32_t R0 = 0;
+  for (uint32_t B = 0; B < T; B += 32) {
+    const uint32_t sb = pre - B;
+    const uint32_t M = __reduce_or_sync(0xffffffffu, (len > 0 && sb < 32u) ? (1u << sb) : 0u);
+    const uint32_t rank = R0 + __popc(M & (0xffffffffu >> (31 - lane)));
+    R0 += __popc(M);
+    const uint32_t t = B + (uint32_t)lane;
+    if (t < T) {
+      const uint2 o = S.own[wi][S.tbl[wi][(rank - 1u) & 31u]];
+      dir[o.x + t] = o.y;
+    }
+  }
+  __syncwarp();
+}
+
+// empty bands: both entries = band start
+__device__ __forceinline__ void dir_empty_bands(const BandLayout* lay, int L, uint32_t* dir) {
   if (blockIdx.x == 0 && threadIdx.x < (unsigned)L) {
-    int jj = threadIdx.x;
+    const int jj = threadIdx.x;
     if (lay->count[jj] == 0) {
-      uint32_t off = lay->dir_off[jj], nb = lay->nb[jj];
+      const uint32_t off = lay->dir_off[jj], nb = lay->nb[jj];
       for (uint32_t bb = 0; bb <= nb; ++bb) dir[off + bb] = lay->start[jj];
     }
   }
+}
+
+// Gather of the query records in sorted order (+ the directory when dir != null).
+// Warp-uniform loop: warp-chunk w covers sorted positions [32 w, 32 w + 32).
+// PHILOX: the points are re-derived from Philox(seed, i) (bit-identical to K1,
+// same device code) instead of gathering theta[i], r[i] at random addresses.
+template <bool PHILOX>
+__global__ void __launch_bounds__(256)
+    k_gather(uint32_t n, const double* __restrict__ theta, const double* __restrict__ r,
+             PhiloxPoints gen, const uint32_t* __restrict__ skey,
+             const uint32_t* __restrict__ sidx, const BandLayout* __restrict__ lay, int L,
+             PointRec* __restrict__ pts, uint32_t* __restrict__ sid2, uint32_t* __restrict__ dir,
+             int seq_ids) {
+  __shared__ DirSmem S;
+  if (dir) {
+    dir_smem_init(S, lay, L);
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); (uint64_t)w * 32 < n;
+       w += nwarps) {
+    const uint32_t k = w * 32 + (uint32_t)lane;
+    uint32_t key = 0;
+    if (k < n) {
+      key = __ldg(skey + k);
+      const uint32_t i = __ldg(sidx + k);
+      double th, rr;
+      if (PHILOX) {
+        words_to_point(vertex_words(gen.seed, i), gen.two_over_alpha, gen.half_span, gen.R, th, rr);
+      } else {
+        th = theta[i];
+        rr = r[i];
+      }
+      put_doubled(k, key, lay, point_rec(th, rr), seq_ids ? k : i, pts, sid2);
+    }
+    if (dir) dir_warp(w, n, skey, key, S, dir);
+  }
+  if (dir) dir_empty_bands(lay, L, dir);
 }
 
 // ---- query order (sector-major) ----
@@ -195,12 +214,12 @@ cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
   if (gen)
-    k_gather_philox<<<blocks, 256, 0, st>>>(n, gen->seed, gen->two_over_alpha, gen->half_span,
-                                            gen->R, skey, sidx, lay, pts, sid2, seq_ids);
+    k_gather<true><<<blocks, 256, 0, st>>>(n, theta, r, *gen, skey, sidx, lay, L, pts, sid2, dir,
+                                           seq_ids);
   else
-    k_gather<<<blocks, 256, 0, st>>>(n, theta, r, skey, sidx, lay, pts, sid2, seq_ids);
-  if (dir) k_directory<<<blocks, 256, 0, st>>>(n, skey, lay, L, dir);
-  if (launches) *launches += dir ? 2 : 1;
+    k_gather<false><<<blocks, 256, 0, st>>>(n, theta, r, PhiloxPoints{}, skey, sidx, lay, L, pts,
+                                            sid2, dir, seq_ids);
+  if (launches) *launches += 1;
   return cudaGetLastError();
 }
 
