@@ -55,10 +55,13 @@ __global__ void __launch_bounds__(RS_RADIX) k_rs_digit_start(int P, const uint32
 }
 
 #ifndef RHG_RS_MINB
-#define RHG_RS_MINB 4
+#define RHG_RS_MINB 5
 #endif
 // Look-back status of (tile, digit): bits 62-63 flag (0 not yet, 1 tile count,
 // 2 inclusive prefix over tiles), bits 0-61 the value.
+#ifndef RHG_RS_VAL_SMEM
+#define RHG_RS_VAL_SMEM 1
+#endif
 #ifndef RHG_RS_BALLOT_MATCH
 #define RHG_RS_BALLOT_MATCH 1
 #endif
@@ -96,14 +99,27 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
   const uint32_t tbase = tile * RS_TILE;
   const uint32_t wbase = tbase + w * (32 * RS_ITEMS);
   static_assert(RS_ITEMS % 2 == 0 && 32 * RS_ITEMS <= 65536, "two 16-bit ranks per register");
-  uint32_t key[RS_ITEMS], val[RS_ITEMS], loc2[RS_ITEMS / 2];  // rank in the warp's digit run
+  uint32_t key[RS_ITEMS], loc2[RS_ITEMS / 2];  // rank in the warp's digit run
   const uint32_t lt = (1u << lane) - 1u;
+#if RHG_RS_VAL_SMEM
+  // values parked in shared memory at their input slots until the scatter (fewer
+  // live registers through the ranking and the look-back)
+  uint32_t* vpark = sval + w * (32 * RS_ITEMS);
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    const uint32_t i = wbase + it * 32 + lane;
+    key[it] = i < n ? __ldg(kin + i) : 0u;
+    vpark[it * 32 + lane] = i < n ? __ldg(vin + i) : 0u;
+  }
+#else
+  uint32_t val[RS_ITEMS];
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {  // all loads in flight before the ranking chain
     const uint32_t i = wbase + it * 32 + lane;
     key[it] = i < n ? __ldg(kin + i) : 0u;
     val[it] = i < n ? __ldg(vin + i) : 0u;
   }
+#endif
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const uint32_t i = wbase + it * 32 + lane;
@@ -186,6 +202,12 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     gbase[d] = dstart[d] + (uint32_t)excl;
   }
   __syncthreads();
+#if RHG_RS_VAL_SMEM
+  uint32_t val[RS_ITEMS];
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) val[it] = vpark[it * 32 + lane];
+  __syncthreads();
+#endif
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const uint32_t i = wbase + it * 32 + lane;
