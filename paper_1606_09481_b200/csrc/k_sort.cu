@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
     // look back over up to kLb earlier tiles per round (their words loaded together),
     // summing tile counts until an inclusive prefix
 #ifndef RHG_RS_LOOKBACK
-#define RHG_RS_LOOKBACK 4
+#define RHG_RS_LOOKBACK 1
 #endif
     constexpr uint32_t kLb = RHG_RS_LOOKBACK;
     unsigned long long excl = 0;
