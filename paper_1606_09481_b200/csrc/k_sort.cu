@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(RS_RADIX) k_rs_digit_start(int P, const uint32
 #endif
 // Look-back status of (tile, digit): bits 62-63 flag (0 not yet, 1 tile count,
 // 2 inclusive prefix over tiles), bits 0-61 the value.
+#ifndef RHG_RS_SPIN_NS
+#define RHG_RS_SPIN_NS 0
+#endif
 #ifndef RHG_RS_VAL_SMEM
 #define RHG_RS_VAL_SMEM 1
 #endif
@@ -179,7 +182,12 @@ __global__ void __launch_bounds__(RS_THREADS, RHG_RS_MINB)
       for (uint32_t j = 0; j < kLb; ++j) {
         if (done || j >= k) continue;
         const volatile unsigned long long* o = status + (size_t)(t2 - 1 - j) * RS_RADIX + d;
-        while ((v[j] & ~kRsVal) == 0ull) v[j] = *o;
+        while ((v[j] & ~kRsVal) == 0ull) {
+#if RHG_RS_SPIN_NS
+          __nanosleep(RHG_RS_SPIN_NS);  // back off: the spinning warps' polls take issue slots
+#endif
+          v[j] = *o;
+        }
         excl += v[j] & kRsVal;
         done = (v[j] & ~kRsVal) == kRsIncl;
       }
