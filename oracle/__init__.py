@@ -80,6 +80,19 @@ def lib():
         L.orc_row_ties.restype = ctypes.c_int64
         L.orc_row_ties.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double, ctypes.c_uint32,
                                    _u32p, _u8p, ctypes.c_uint64]
+        L.orc_angle_order.argtypes = [ctypes.c_uint64, _f64p, _u32p, _u32p]
+        L.orc_sweep_count_ordered.restype = ctypes.c_int64
+        L.orc_sweep_count_ordered.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double,
+                                              _u32p, _u32p, ctypes.c_uint64, ctypes.c_uint64,
+                                              _u64p]
+        L.orc_sweep_csr.restype = ctypes.c_int64
+        L.orc_sweep_csr.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double, _u64p, _u32p,
+                                    ctypes.c_uint64, _u32p, _u8p, ctypes.c_uint64, _u64p, _u64p]
+        L.orc_sweep_digest.restype = ctypes.c_int64
+        L.orc_sweep_digest.argtypes = [ctypes.c_uint64, _f64p, _f64p, ctypes.c_double, _u64p,
+                                       _u64p, _u32p, _u8p, ctypes.c_uint64, _u64p]
+        L.orc_mix64.restype = ctypes.c_uint64
+        L.orc_mix64.argtypes = [ctypes.c_uint64]
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_radius_from_C.restype = ctypes.c_double
         L.orc_radius_from_C.argtypes = [ctypes.c_double] * 2
@@ -231,6 +244,82 @@ def sweep_count(theta, r, R, id_lo, id_hi):
     m = lib().orc_sweep_count(len(theta), _p(theta, _f64p), _p(r, _f64p), R, id_lo, id_hi,
                               ctypes.byref(t))
     return int(m), int(t.value)
+
+
+def angle_order(theta):
+    """(order, pos): ids sorted by (theta, id) and the inverse (uint32)."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    n = len(theta)
+    order = np.zeros(n, dtype=np.uint32)
+    pos = np.zeros(n, dtype=np.uint32)
+    lib().orc_angle_order(n, _p(theta, _f64p), _p(order, _u32p), _p(pos, _u32p))
+    return order, pos
+
+
+def sweep_count_ordered(theta, r, R, order, pos, id_lo, id_hi):
+    """Count-only sweep of owners [id_lo, id_hi) on a given angular order:
+    (edges, tests)."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    t = ctypes.c_uint64()
+    m = lib().orc_sweep_count_ordered(len(theta), _p(theta, _f64p), _p(r, _f64p), R,
+                                      _p(order, _u32p), _p(pos, _u32p), id_lo, id_hi,
+                                      ctypes.byref(t))
+    return int(m), int(t.value)
+
+
+class CSR:
+    """Oracle CSR: both directions, rows ascending; plus near-tie pairs."""
+
+    def __init__(self, row_ptr, col, ties, tie_edge):
+        self.row_ptr, self.col, self.ties, self.tie_edge = row_ptr, col, ties, tie_edge
+
+
+def sweep_csr(theta, r, R, cap_hint=None) -> CSR:
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    n = len(theta)
+    cap = max(int(cap_hint or 16 * n + 1024), 16)
+    tcap = 1 << 16
+    while True:
+        rp = np.zeros(n + 1, dtype=np.uint64)
+        col = np.empty(cap, dtype=np.uint32)
+        ties = np.zeros((tcap, 2), dtype=np.uint32)
+        te = np.zeros(tcap, dtype=np.uint8)
+        nt, need = ctypes.c_uint64(), ctypes.c_uint64()
+        m = lib().orc_sweep_csr(n, _p(theta, _f64p), _p(r, _f64p), R, _p(rp, _u64p),
+                                _p(col, _u32p), cap, _p(ties, _u32p), _p(te, _u8p), tcap,
+                                ctypes.byref(nt), ctypes.byref(need))
+        if m >= 0:
+            return CSR(rp, col[:m], ties[: nt.value].copy(), te[: nt.value].astype(bool))
+        cap = max(cap, int(need.value) + 16)
+        tcap = max(tcap, int(nt.value) + 16)
+        del col
+
+
+def sweep_digest(theta, r, R):
+    """(m, deg[n] uint64, digest[n] uint64, ties, tie_edge): per-vertex degree and
+    sum of mix64(neighbour) mod 2^64 of the sweep's edge set."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    n = len(theta)
+    tcap = 1 << 16
+    while True:
+        deg = np.zeros(n, dtype=np.uint64)
+        dig = np.zeros(n, dtype=np.uint64)
+        ties = np.zeros((tcap, 2), dtype=np.uint32)
+        te = np.zeros(tcap, dtype=np.uint8)
+        nt = ctypes.c_uint64()
+        m = lib().orc_sweep_digest(n, _p(theta, _f64p), _p(r, _f64p), R, _p(deg, _u64p),
+                                   _p(dig, _u64p), _p(ties, _u32p), _p(te, _u8p), tcap,
+                                   ctypes.byref(nt))
+        if nt.value <= tcap:
+            return int(m), deg, dig, ties[: nt.value].copy(), te[: nt.value].astype(bool)
+        tcap = int(nt.value) + 16
+
+
+def mix64(w: int) -> int:
+    return int(lib().orc_mix64(w))
 
 
 def rows(theta, r, R, queries):

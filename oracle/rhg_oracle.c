@@ -13,9 +13,10 @@
  *   PAPER.md:L (section / equation / algorithm line)  -- /root/reference/PAPER.md
  *   DESIGN.md "Reading Zk"                            -- where the paper is silent
  *
- * Parity status of each function is listed in DESIGN.md ("Oracle pins").  Nothing
- * here is "parity unpinned" except orc_sampled_rows at sizes the tests cannot
- * brute-force completely (that is a sampling of the pinned brute-force predicate).
+ * Parity status of each function is listed in DESIGN.md §10 ("Oracle pins"); every
+ * exported function has a CPU test in tests/test_oracle.py that checks it against
+ * something other than itself (brute force, 50/60-digit mpmath of the paper's
+ * literal formulas, NVIDIA's Philox header, closed forms).
  */
 #include <math.h>
 #include <quadmath.h>
@@ -500,6 +501,213 @@ ORC_API int64_t orc_sweep_count(uint64_t n, const double *theta, const double *r
   free(s);
   free(pos);
   if (tests) *tests = t;
+  return (int64_t)m;
+}
+
+/* ------------------------------------------------------------------------ */
+/* (2c) The sweep of (2), split into its two steps so that they can be timed  */
+/* and reused: the angular order of all points (one qsort by (theta, id)),    */
+/* then per owner vertex v the scan of +-window(r_v, r_v) (padded) over the   */
+/* circle, testing partners with larger (r, id) -- exactly the search and     */
+/* decision of (2).  Positions are uint32 (n < 2^32).                         */
+/* ------------------------------------------------------------------------ */
+ORC_API void orc_angle_order(uint64_t n, const double *theta, uint32_t *order, uint32_t *pos) {
+  orc_ang *s = malloc((n ? n : 1) * sizeof(orc_ang));
+  for (uint64_t i = 0; i < n; ++i) {
+    s[i].theta = theta[i];
+    s[i].id = (uint32_t)i;
+  }
+  qsort(s, n, sizeof(orc_ang), cmp_ang);
+  for (uint64_t k = 0; k < n; ++k) {
+    order[k] = s[k].id;
+    pos[s[k].id] = (uint32_t)k;
+  }
+  free(s);
+}
+
+enum { SW_COUNT = 0, SW_DEG = 1, SW_FILL = 2, SW_DIGEST = 3 };
+
+typedef struct {
+  uint64_t n;
+  const double *theta, *r;
+  const uint32_t *order, *pos;
+  orc_thresh th;
+  /* outputs, by mode */
+  uint64_t *deg;     /* SW_DEG: degree (both endpoints) */
+  uint64_t *cursor;  /* SW_FILL: next free slot of each row */
+  uint32_t *col;     /* SW_FILL */
+  uint64_t *dig;     /* SW_DIGEST: sum of orc_mix64(neighbour id) */
+  uint32_t *ties;    /* SW_DEG / SW_DIGEST: near-tie pairs (u < v) */
+  uint8_t *tie_edge;
+  uint64_t tie_cap, *n_ties;
+} sweep_ctx;
+
+/* Order-independent digest of a neighbour set: sum over w of mix(w) mod 2^64,
+ * mix = the SplitMix64 finaliser of w.  Test infrastructure (a checksum of the
+ * output, not part of the method). */
+ORC_API uint64_t orc_mix64(uint64_t w) {
+  uint64_t z = w * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* Scan owner v; returns its edges, adds its tests to *tests. */
+static uint64_t sweep_one(const sweep_ctx *cx, uint64_t v, int mode, uint64_t *tests) {
+  const double rv = cx->r[v], tv = cx->theta[v];
+  const double wpad = orc_window(rv, rv, cx->th.R) * (1.0 + 1e-9) + 1e-12;
+  const int full = wpad >= M_PI;
+  const uint64_t n = cx->n, p = cx->pos[v];
+  uint64_t m = 0, t = 0;
+  for (int dir = 0; dir < (full ? 1 : 2); ++dir) {
+    for (uint64_t step = 1; step < n; ++step) {
+      const uint64_t k = dir == 0 ? (p + step) % n : (p + n - step) % n;
+      const uint32_t u = cx->order[k];
+      if (!full && orc_angle_between(tv, cx->theta[u]) > wpad) break;
+      if (u == (uint32_t)v) break;
+      if (cx->r[u] < rv || (cx->r[u] == rv && u < (uint32_t)v)) continue;
+      int tie = 0;
+      const int e = orc_decide(&cx->th, tv, rv, cx->theta[u], cx->r[u], &tie);
+      ++t;
+      m += e;
+      if (tie && (mode == SW_DEG || mode == SW_DIGEST)) {
+        uint64_t slot;
+#pragma omp atomic capture
+        slot = (*cx->n_ties)++;
+        if (slot < cx->tie_cap) {
+          cx->ties[2 * slot] = (uint32_t)v < u ? (uint32_t)v : u;
+          cx->ties[2 * slot + 1] = (uint32_t)v < u ? u : (uint32_t)v;
+          cx->tie_edge[slot] = (uint8_t)e;
+        }
+      }
+      if (!e) continue;
+      if (mode == SW_DEG || mode == SW_DIGEST) {
+#pragma omp atomic
+        cx->deg[v] += 1;
+#pragma omp atomic
+        cx->deg[u] += 1;
+      }
+      if (mode == SW_DIGEST) {
+        const uint64_t a = orc_mix64(u), b = orc_mix64(v);
+#pragma omp atomic
+        cx->dig[v] += a;
+#pragma omp atomic
+        cx->dig[u] += b;
+      }
+      if (mode == SW_FILL) {
+        uint64_t sv, su;
+#pragma omp atomic capture
+        sv = cx->cursor[v]++;
+#pragma omp atomic capture
+        su = cx->cursor[u]++;
+        cx->col[sv] = u;
+        cx->col[su] = (uint32_t)v;
+      }
+    }
+  }
+  *tests += t;
+  return m;
+}
+
+static sweep_ctx sweep_setup(uint64_t n, const double *theta, const double *r, double R,
+                             const uint32_t *order, const uint32_t *pos) {
+  sweep_ctx cx;
+  memset(&cx, 0, sizeof(cx));
+  cx.n = n;
+  cx.theta = theta;
+  cx.r = r;
+  cx.order = order;
+  cx.pos = pos;
+  cx.th = orc_make_thresh(R);
+  return cx;
+}
+
+/* Count-only sweep over the owners with id in [id_lo, id_hi), on a given angular
+ * order (orc_angle_order).  Same search and decision as (2); *tests = candidate
+ * pairs decided.  Used to time the oracle with its sort step separated. */
+ORC_API int64_t orc_sweep_count_ordered(uint64_t n, const double *theta, const double *r, double R,
+                                        const uint32_t *order, const uint32_t *pos, uint64_t id_lo,
+                                        uint64_t id_hi, uint64_t *tests) {
+  sweep_ctx cx = sweep_setup(n, theta, r, R, order, pos);
+  uint64_t m = 0, t = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : m, t)
+  for (int64_t v = (int64_t)id_lo; v < (int64_t)id_hi; ++v) m += sweep_one(&cx, (uint64_t)v, SW_COUNT, &t);
+  if (tests) *tests = t;
+  return (int64_t)m;
+}
+
+static int cmp_u32(const void *a, const void *b) {
+  uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+  return x < y ? -1 : (x > y);
+}
+
+/* (2d) The sweep's edge set as a CSR: both directions, no self-loops, every row
+ * in ascending id order (the same set as (2); the CSR of SURVEY.md §8(a) output
+ * semantics, rows canonicalised).  Pass 1 counts degrees (and collects the
+ * near-tie pairs), pass 2 fills the rows, then each row is sorted.  Returns the
+ * directed entry count, or -1 if it exceeds cap (*needed = the count). */
+ORC_API int64_t orc_sweep_csr(uint64_t n, const double *theta, const double *r, double R,
+                              uint64_t *row_ptr, uint32_t *col, uint64_t cap, uint32_t *ties,
+                              uint8_t *tie_edge, uint64_t tie_cap, uint64_t *n_ties,
+                              uint64_t *needed) {
+  uint32_t *order = malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t *pos = malloc((n ? n : 1) * sizeof(uint32_t));
+  orc_angle_order(n, theta, order, pos);
+  sweep_ctx cx = sweep_setup(n, theta, r, R, order, pos);
+  uint64_t *deg = calloc(n ? n : 1, sizeof(uint64_t));
+  uint64_t nt = 0, t = 0;
+  cx.deg = deg;
+  cx.ties = ties;
+  cx.tie_edge = tie_edge;
+  cx.tie_cap = tie_cap;
+  cx.n_ties = &nt;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : t)
+  for (int64_t v = 0; v < (int64_t)n; ++v) sweep_one(&cx, (uint64_t)v, SW_DEG, &t);
+  row_ptr[0] = 0;
+  for (uint64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + deg[i];
+  *needed = row_ptr[n];
+  *n_ties = nt;
+  if (row_ptr[n] > cap || nt > tie_cap) {
+    free(order); free(pos); free(deg);
+    return -1;
+  }
+  memcpy(deg, row_ptr, n * sizeof(uint64_t)); /* deg becomes the fill cursor */
+  cx.cursor = deg;
+  cx.col = col;
+  t = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : t)
+  for (int64_t v = 0; v < (int64_t)n; ++v) sweep_one(&cx, (uint64_t)v, SW_FILL, &t);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t v = 0; v < (int64_t)n; ++v)
+    qsort(col + row_ptr[v], row_ptr[v + 1] - row_ptr[v], sizeof(uint32_t), cmp_u32);
+  free(order); free(pos); free(deg);
+  return (int64_t)row_ptr[n];
+}
+
+/* (2e) Per-vertex degree and neighbour-set digest (orc_mix64 sum) of the sweep's
+ * edge set, in one pass: a full-graph comparison at sizes where the edge list
+ * itself is not materialised on the host (n = 1e8).  Near-tie pairs collected as
+ * in (2d).  Returns the undirected edge count. */
+ORC_API int64_t orc_sweep_digest(uint64_t n, const double *theta, const double *r, double R,
+                                 uint64_t *deg, uint64_t *dig, uint32_t *ties, uint8_t *tie_edge,
+                                 uint64_t tie_cap, uint64_t *n_ties) {
+  uint32_t *order = malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t *pos = malloc((n ? n : 1) * sizeof(uint32_t));
+  orc_angle_order(n, theta, order, pos);
+  sweep_ctx cx = sweep_setup(n, theta, r, R, order, pos);
+  memset(deg, 0, n * sizeof(uint64_t));
+  memset(dig, 0, n * sizeof(uint64_t));
+  uint64_t nt = 0, t = 0, m = 0;
+  cx.deg = deg;
+  cx.dig = dig;
+  cx.ties = ties;
+  cx.tie_edge = tie_edge;
+  cx.tie_cap = tie_cap;
+  cx.n_ties = &nt;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : t, m)
+  for (int64_t v = 0; v < (int64_t)n; ++v) m += sweep_one(&cx, (uint64_t)v, SW_DIGEST, &t);
+  *n_ties = nt;
+  free(order); free(pos);
   return (int64_t)m;
 }
 
