@@ -60,10 +60,14 @@ typedef enum {
 /* Tuning knobs.  The edge set does not depend on them (DESIGN.md "Why parity is
    layout-free"); they only move work between window evaluations and tests. */
 typedef struct {
-  int num_bands;     /* L, number of slabs; 0 -> ceil(log2 n) (Z7) */
-  double band_ratio; /* p, geometric width ratio; 0 -> 0.9 */
-  uint32_t heavy_threshold; /* candidates of one (vertex, slab) range above which the range is
-                               split across warps; 0 -> library default */
+  int num_bands;     /* L, number of slabs (1..32); 0 -> min(16, ceil(ln n)) ("log n" slabs,
+                        PAPER.md:108, base unstated; Z7) */
+  double band_ratio; /* p, geometric width ratio in (0, 1); 0 -> 0.85 (the paper's 0.9,
+                        PAPER.md:116-124, costs more tests with L capped at 16; Z7) */
+  uint32_t heavy_threshold; /* hub selection: a slab's vertices whose expected candidate
+                               count (upper bound over the slab, all slabs' windows) exceeds
+                               this are hubs, whose candidate sequences are cut into chunks
+                               spread over all warps (DESIGN.md §1 a7); 0 -> 1024 */
   /* Sharding: with shard_count = N > 1 the call emits only
      the edges owned by shard shard_index: the rows (CSR) or the outward edges (list)
      of 1/N of the light query order and 1/N of the hub vertices.  Every shard samples

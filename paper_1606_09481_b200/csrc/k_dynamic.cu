@@ -53,7 +53,7 @@ __global__ void k_move(uint64_t n, double* __restrict__ theta, double* __restric
 static int grid_for(uint64_t n) {
   uint64_t b = (n + 255) / 256;
   if (b < 1) b = 1;
-  return (int)(b > 148u * 16u ? 148u * 16u : b);
+  return (int)(b > (uint32_t)num_sms() * 16u ? (uint32_t)num_sms() * 16u : b);
 }
 
 cudaError_t launch_movement_init(uint64_t n, uint64_t seed, double phi_lo, double phi_hi,

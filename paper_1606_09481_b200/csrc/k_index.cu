@@ -211,7 +211,7 @@ cudaError_t launch_build_index(uint32_t n, const double* theta, const double* r,
                                const PhiloxPoints* gen, int seq_ids, cudaStream_t st,
                                int* launches) {
   int blocks = (int)((n + 255) / 256);
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > (uint32_t)num_sms() * 32) blocks = (uint32_t)num_sms() * 32;
   if (blocks < 1) blocks = 1;
   if (gen)
     k_gather<true><<<blocks, 256, 0, st>>>(n, theta, r, *gen, skey, sidx, lay, L, pts, sid2, dir,

@@ -1120,7 +1120,7 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
 cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                               const BandConst& bc, void* scan_tmp, cudaStream_t st, int* launches) {
   uint32_t blocks = (uint32_t)((bc.heavy_cap + HV_WARPS - 1) / HV_WARPS);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > (uint32_t)num_sms() * 8) blocks = (uint32_t)num_sms() * 8;
   if (blocks < 1) blocks = 1;
   if (fmt == RHG_CSR) k_heavy_ranges<RHG_CSR><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);
   else k_heavy_ranges<RHG_EDGES_UNDIRECTED><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);
@@ -1128,7 +1128,7 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
                                              scan_tmp, &ha.meta->cand, st, launches);
   if (e != cudaSuccess) return e;
   k_heavy_chunk_size<<<1, 1, 0, st>>>(ha);
-  k_heavy_chunk_counts<<<148 * 4, 256, 0, st>>>(ha);
+  k_heavy_chunk_counts<<<num_sms() * 4, 256, 0, st>>>(ha);
   e = exclusive_scan_u32_u64_dev(ha.vcap, &ha.meta->nvtx, ha.cc, ha.choff, scan_tmp,
                                  &ha.meta->nchunks, st, launches);
   if (e != cudaSuccess) return e;
@@ -1139,7 +1139,7 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
 
 cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                          const BandConst& bc, cudaStream_t st) {
-  const uint32_t blocks = 148 * RHG_HV_BLOCKS;
+  const uint32_t blocks = (uint32_t)num_sms() * RHG_HV_BLOCKS;
   if (mode == QM_COUNT) {
     if (fmt == RHG_CSR) k_heavy<QM_COUNT, RHG_CSR><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);
     else k_heavy<QM_COUNT, RHG_EDGES_UNDIRECTED><<<blocks, HV_THREADS, 0, st>>>(qa, ha, bc);

@@ -169,14 +169,14 @@ static int grid_for(uint64_t n, int threads, int max_blocks) {
 
 cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out,
                                 cudaStream_t st) {
-  k_philox_words<<<grid_for(count, 256, 148 * 16), 256, 0, st>>>(seed, i0, count, out);
+  k_philox_words<<<grid_for(count, 256, num_sms() * 16), 256, 0, st>>>(seed, i0, count, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sample(uint64_t n, const PhiloxPoints& gen, const BandConst& bc, double* theta,
                           double* r, uint32_t* keys, uint32_t* idx, uint32_t* band_hist,
                           cudaStream_t st) {
-  k_sample<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, gen.seed, gen.two_over_alpha,
+  k_sample<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(n, gen.seed, gen.two_over_alpha,
                                                        gen.half_span, bc, theta, r, keys, idx,
                                                        band_hist);
   return cudaGetLastError();
@@ -185,7 +185,7 @@ cudaError_t launch_sample(uint64_t n, const PhiloxPoints& gen, const BandConst& 
 cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const double* r,
                                     const BandConst& bc, uint32_t* keys, uint32_t* idx,
                                     uint32_t* band_hist, DevScalars* sc, cudaStream_t st) {
-  k_keys_from_points<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, theta, r, bc, keys, idx,
+  k_keys_from_points<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(n, theta, r, bc, keys, idx,
                                                                  band_hist, sc);
   return cudaGetLastError();
 }

@@ -4,6 +4,8 @@
 // Paper: "sort points in b by their angular coordinates" (Alg. 1 lines 11-12,
 // PAPER.md:153-155).  One global sort by (band, angle) yields every band as a
 // contiguous, angle-sorted segment (the slabs b_i of PAPER.md:192-197).
+#include <atomic>
+
 #include "rhg_internal.cuh"
 
 namespace rhg {
@@ -400,12 +402,15 @@ size_t radix_sort_tmp_bytes(uint64_t n) {
 }
 
 // opt in to > 48 KB of dynamic shared memory once (outside any stream capture)
+// (the attribute is per device: one flag per device, set atomically)
 cudaError_t radix_sort_prepare() {
-  static bool done = false;
-  if (done) return cudaSuccess;
+  static std::atomic<bool> done[64];
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) d = 0;
+  if (done[d].load(std::memory_order_acquire)) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(k_rs_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              2 * RS_TILE * (int)sizeof(uint32_t));
-  if (e == cudaSuccess) done = true;
+  if (e == cudaSuccess) done[d].store(true, std::memory_order_release);
   return e;
 }
 
@@ -420,10 +425,12 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
   uint32_t* dstart = ghist + 4 * RS_RADIX;
   uint32_t* tickets = dstart + 4 * RS_RADIX;
   unsigned long long* status = (unsigned long long*)(tickets + 8);  // 32-byte aligned
-  cudaError_t e = cudaMemsetAsync(tmp, 0, radix_sort_tmp_bytes(n) - 256, st);
+  // counts, starts, tickets and the look-back words of the P passes that run
+  const size_t zero = (size_t)((char*)(status + (size_t)P * G * RS_RADIX) - (char*)tmp);
+  cudaError_t e = cudaMemsetAsync(tmp, 0, zero, st);
   if (e != cudaSuccess) return e;
   uint32_t hb = (n + RS_THREADS * 16 - 1) / (RS_THREADS * 16);
-  if (hb > 148 * 8) hb = 148 * 8;
+  if (hb > (uint32_t)num_sms() * 8) hb = (uint32_t)num_sms() * 8;
   k_rs_hist_all<<<hb, RS_THREADS, 0, st>>>(n, keys_a, P, ghist);
   k_rs_digit_start<<<1, RS_RADIX, 0, st>>>(P, ghist, dstart);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
@@ -439,8 +446,10 @@ cudaError_t radix_sort(uint32_t n, uint32_t* keys_a, uint32_t* vals_a, uint32_t*
   }
   if (launches) *launches += 2 + P;
   if (P & 1) {  // result must land in (keys_a, vals_a)
-    cudaMemcpyAsync(keys_a, ki, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(vals_a, vi, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(keys_a, ki, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(vals_a, vi, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

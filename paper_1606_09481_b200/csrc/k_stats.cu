@@ -120,7 +120,7 @@ cudaError_t launch_graph_stats(uint32_t n, int fmt, const uint64_t* row_ptr, con
   uint32_t* deg = (uint32_t*)((char*)ws + ((sizeof(StatsAcc) + 255) & ~(size_t)255));
   cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(StatsAcc), st);
   if (e != cudaSuccess) return e;
-  const int blocks = 148 * 8;
+  const int blocks = num_sms() * 8;
   if (fmt != RHG_CSR) {
     if ((e = cudaMemsetAsync(deg, 0, 4ull * n, st)) != cudaSuccess) return e;
     k_stats_pair_degrees<<<blocks, ST_THREADS, 0, st>>>(m, pairs, deg);

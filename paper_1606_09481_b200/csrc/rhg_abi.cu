@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include <vector>
@@ -219,15 +220,19 @@ int& last_cuda_error_line() {
   return l;
 }
 
-std::mutex g_pin_mu;
-DevScalars* g_pin = nullptr;  // page-locked readback slot
-
-DevScalars* pinned_scalars() {
-  std::lock_guard<std::mutex> g(g_pin_mu);
-  if (!g_pin) {
-    if (cudaMallocHost(&g_pin, sizeof(DevScalars)) != cudaSuccess) g_pin = nullptr;
+// Page-locked readback slot, one per host thread (a process-wide slot
+// let concurrent callers read each other's totals).  Its address is stable per
+// thread, so the CUDA graphs cached per thread (graph_cache) stay valid.
+struct PinnedSlot {
+  DevScalars* p = nullptr;
+  ~PinnedSlot() {
+    if (p) cudaFreeHost(p);
   }
-  return g_pin;
+};
+DevScalars* pinned_scalars() {
+  static thread_local PinnedSlot slot;
+  if (!slot.p && cudaMallocHost(&slot.p, sizeof(DevScalars)) != cudaSuccess) slot.p = nullptr;
+  return slot.p;
 }
 
 #define CK(x)                                  \
@@ -253,9 +258,15 @@ struct SideStream {
          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess;
   }
 };
+// one side stream (and its events) per thread and device: the caller's stream
+// belongs to the current device
+constexpr int kMaxDevices = 64;
 SideStream& side_stream() {
-  static thread_local SideStream ss;
-  return ss;
+  static thread_local SideStream* ss[kMaxDevices] = {};
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  if (!ss[d]) ss[d] = new SideStream();
+  return *ss[d];
 }
 
 struct Timer {
@@ -613,6 +624,21 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
 }
 
 }  // namespace
+
+namespace rhg {
+int num_sms() {
+  static std::atomic<int> cache[kMaxDevices];
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  int v = cache[d].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+}  // namespace rhg
 
 #define RHG_EXPORT __attribute__((visibility("default")))
 

@@ -175,6 +175,10 @@ struct PhiloxPoints {
   double two_over_alpha, half_span, R;
 };
 
+// Streaming multiprocessors of the current device (cudaDevAttrMultiProcessorCount,
+// cached per device): grids are sized in multiples of it.
+int num_sms();
+
 // ---- launch wrappers (each returns cudaError_t of the launch) ----
 cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint32_t* out,
                                 cudaStream_t st);
