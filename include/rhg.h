@@ -109,7 +109,8 @@ typedef struct {
   uint64_t candidates;     /* candidate (vertex, point) pairs tested exactly in the count pass */
   uint64_t certain;        /* edges accepted by the certified inner window, without a test */
   uint64_t launches;       /* kernels launched by this call                                 */
-  uint64_t emit_retested;  /* 1 if the emit pass had to re-run the tests (bit buffer overflow) */
+  uint64_t emit_retested;  /* light warps (32 vertices each) whose test bits did not fit and
+                              whose emit pass re-runs their tests                             */
 } rhg_timing;
 
 typedef struct {

@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     const bool anyover = __any_sync(FULL, over);
     if (lane == 0) {
       A.warp_over[g] = anyover ? 1u : 0u;
-      if (anyover) atomicOr(&A.sc->bit_overflow, 1u);
+      if (anyover) atomicAdd(&A.sc->bit_overflow, 1u);  // warps whose emit re-tests
     }
     if (A.stats) {  // timing statistics only
       const unsigned long long tw = warp_incl((unsigned long long)tested);

@@ -618,7 +618,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     t->candidates = hs.candidates;
     t->certain = hs.certain;
     t->launches = (uint64_t)launches;
-    t->emit_retested = hs.bit_overflow ? 1 : 0;
+    t->emit_retested = hs.bit_overflow;
   }
   return RHG_OK;
 }

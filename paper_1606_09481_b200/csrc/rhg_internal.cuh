@@ -96,7 +96,7 @@ struct DevScalars {
   unsigned long long certain;      // edges accepted by the certified inner window (no test)
   unsigned long long bit_words;    // candidate-bit words allocated by the count pass
   unsigned int domain_error;       // a point outside the disk
-  unsigned int bit_overflow;       // bit buffer too small -> emit re-tests
+  unsigned int bit_overflow;       // light warps whose bit buffer was too small (emit re-tests)
   unsigned int dbg_line;           // RHG_BOUNDS builds: first failed check (line, values)
   unsigned long long dbg[3];
 };
