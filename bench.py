@@ -14,11 +14,11 @@ SURVEY §8(a) contract); the same workload with ids in (slab, angle) order
 (vertex_order 1, perm output) is timed beside it ("other_vertex_order"), and the
 five BASELINE configs are reported at 1 GPU ("configs_1gpu", outside the timed loop).
 
-Prints ONE JSON line (rank 0).  N > 1 (torchrun): by default every rank generates
-its own independent graph (seed 3 + rank): replicas, weak scaling, no data-path
-collective.  --mode shard: one graph, each rank emits the rows of 1/N of the
-vertices and the ranks all_gather one 8-byte edge count (NCCL) per step: strong
-scaling.
+Prints ONE JSON line (rank 0).  N > 1 (torchrun): by default ONE graph is sharded
+over the ranks: every rank samples, sorts and indexes all points,
+emits the rows of an equal share of the estimated work, and the ranks all_gather
+one 8-byte edge count (NCCL) per step: strong scaling.  --mode replicas: every rank
+generates its own independent graph (seed 3 + rank), weak scaling.
 --impl reference times the CPU oracle (oracle/, C + OpenMP) on the host cores.
 """
 from __future__ import annotations
@@ -431,6 +431,7 @@ def run_ours(args):
         configs = five_configs(rhg, torch, dev, flush, args.order, hbm_peak, 0 if args.no_graph else 1)
     if rank == 0 and world == 1 and not args.no_e2e:
         e2e = measure_e2e(rhg, torch, c, seed, dev, ws, cap, args, opts)
+        e2e["from_points"] = measure_e2e_points(rhg, torch, c, seed, dev, ws, cap, args, opts)
     near = None
     if rank == 0 and world == 1:
         near = near_tie_stats(rhg, torch, c, seed, dev, opts)
@@ -582,6 +583,48 @@ def near_tie_stats(rhg, torch, c, seed, dev, opts):
     return out
 
 
+def measure_e2e_points(rhg, torch, c, seed, dev, ws, cap, args, opts):
+    """The C-ABI call that carries input payload: rhg_generate_from_points with the
+    n points (theta, r: 16 B each) in page-locked HOST memory and the CSR written to
+    page-locked host buffers; both copies are inside the timed region (the library
+    stages them through the workspace on the caller's stream).  The points are the
+    ones rhg_sample_points draws for this config (copied to the host beforehand)."""
+    n = c["n"]
+    a = (c["gamma"] - 1.0) / 2.0
+    R = rhg.target_radius(n, c["kbar"], c["gamma"])
+    th_d, r_d = rhg.sample_points(n, a, R, seed, device=dev)
+    th = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    r = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    th.copy_(th_d)
+    r.copy_(r_d)
+    del th_d, r_d
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+    col = torch.empty(cap, dtype=torch.int32, pin_memory=True)
+    perm = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    bufs = lambda _cap: (row_ptr, col, None, None, None, perm)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return rhg._run(lambda o, s: rhg.lib().rhg_generate_from_points(
+            n, th.data_ptr(), r.data_ptr(), R, o, s), n, c["fmt"], c["kbar"], device=dev,
+            capacity=cap, options=opts, timing=False, workspace=ws, stream=stream,
+            host_buffers=True, want_points=False, sample=False, out_bufs=bufs)
+
+    step()
+    torch.cuda.synchronize()
+    K = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(K):
+        g = step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / K
+    return {"value": (g.num_edges // 2) / dt, "unit": "edges/s", "ms_per_step": dt * 1e3,
+            "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 8 * (n + 1) + 4 * g.num_edges + (4 * n if args.order == 1 else 0),
+            "steps": K, "note": "rhg_generate_from_points, host theta/r in, host CSR out "
+                                "(page-locked), wall clock around K calls"}
+
+
 def measure_e2e(rhg, torch, c, seed, dev, ws, cap, args, opts):
     """Same metric through the public API with HOST (pinned) output buffers: the
     device->host copy of the whole CSR (and of perm for vertex_order 1) is inside
@@ -621,8 +664,9 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
-                    help="N > 1: independent graphs per rank (weak) or one graph sharded (strong)")
+    ap.add_argument("--mode", default="shard", choices=["replicas", "shard"],
+                    help="N > 1: one graph sharded over the ranks (strong scaling, SURVEY "
+                         "§8(e); default) or independent graphs per rank (weak)")
     ap.add_argument("--no-configs", action="store_true", help="skip the five-config report")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of graph replay")
     ap.add_argument("--order", type=int, default=0, choices=[0, 1],

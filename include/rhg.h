@@ -70,7 +70,10 @@ typedef struct {
                                spread over all warps (DESIGN.md §1 a7); 0 -> 1024 */
   /* Sharding: with shard_count = N > 1 the call emits only
      the edges owned by shard shard_index: the rows (CSR) or the outward edges (list)
-     of 1/N of the light query order and 1/N of the hub vertices.  Every shard samples
+     of the query vertices it owns.  Ownership balances the estimated work (expected
+     candidates per vertex): hub vertices are dealt in snake order, the light
+     vertices go in N contiguous ranges of the sector-major order whose work makes up
+     each shard's share (k_shard.cu).  Every shard samples
      and indexes the whole point set; rows of vertices owned by other shards are
      empty, so the N outputs are disjoint and their union is the graph.  Output
      (row contents included) is identical to the unsharded call's for owned vertices.

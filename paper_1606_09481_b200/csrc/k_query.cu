@@ -647,11 +647,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   const uint32_t g = blockIdx.x * QK_WARPS + (threadIdx.x >> 5);  // light warp (of this shard)
   const uint32_t nlight = A.n - A.lay->heavy_end;
   // shard: a contiguous range of the 32-vertex groups of the sector-major order
+  // with an equal share of the estimated work (k_shard.cu)
   const uint32_t ngroups = (nlight + 31u) / 32u;
   uint32_t gbeg = 0, gend = ngroups;
   if (bc.nshards > 1) {
-    gbeg = (uint32_t)shard_begin(ngroups, bc.shard, bc.nshards);
-    gend = (uint32_t)shard_begin(ngroups, bc.shard + 1, bc.nshards);
+    gbeg = min(A.shard_plan->grp_beg, ngroups);
+    gend = min(A.shard_plan->grp_end, ngroups);
   }
   if (gbeg + g >= gend) return;
   const uint32_t idx = (gbeg + g) * 32u + lane;
@@ -899,14 +900,14 @@ __global__ void __launch_bounds__(HV_THREADS)
   const int L = bc.L;
   const uint32_t LS = kRangesPerSlab * (uint32_t)L;
   const bool outward = (FMT == RHG_EDGES_UNDIRECTED);
-  const uint32_t hbeg = (uint32_t)shard_begin(he, bc.shard, bc.nshards);
-  const uint32_t hend = (uint32_t)shard_begin(he, bc.shard + 1, bc.nshards);
+
   for (uint32_t i = gw; i < he; i += TW) {
     const uint32_t qkey = A.skey[i];
     const uint32_t qband = qkey >> kBandShift;
     const PointRec q = A.pts[i + bs.start[qband]];
     const double qinv4s = 0.25 / q.s;
-    const int j = (i >= hbeg && i < hend) ? lane : 32;  // other shards' hubs: no pieces
+    const bool owned = bc.nshards <= 1 || snake(i, bc.nshards) == bc.shard;
+    const int j = owned ? lane : 32;  // other shards' hubs: no pieces
     int64_t lo[6] = {0, 0, 0, 0, 0, 0}, ln[6] = {0, 0, 0, 0, 0, 0};
     uint32_t gbase = 0;
     if (j < L) {
@@ -1117,6 +1118,108 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
   }
 }
 
+// ------------------------------------------------------------------ shard plan
+// Work of the query items for the shard partition (k_shard.cu).
+// Candidates of vertex q in slab j = the outer window's index range (the count the
+// query kernels visit, tested + certain).
+__device__ __forceinline__ uint32_t slab_candidates(const SlabC& S, const PointRec& q, uint32_t qkey,
+                                                    double qinv4s, const BandConst& bc,
+                                                    const uint32_t* __restrict__ dir) {
+  if (S.nj == 0) return 0u;
+  const double h0 = __fma_rn(q.a, S.B0, -__dmul_rn(q.b, S.A0));
+  const double h1 = __fma_rn(q.a, S.B1, -__dmul_rn(q.b, S.A1));
+  SlabWin<int32_t> w;
+  win32(S, (int32_t)(qkey & kQMask), __fma_rn(-h0, h0, bc.T4), __fma_rn(-h1, h1, bc.T4), qinv4s,
+        bc.T4min, dir, w);
+  return w.dq == (1 << 30) ? S.nj : (uint32_t)(w.b - w.a);
+}
+
+// fp32 expected candidates of a vertex: E(r) = sum_k n_k min(1, W(r, c_k)/pi), k >= k0
+__device__ __forceinline__ float expected_candidates(const PointRec& q, const SlabC* scs, int k0,
+                                                     int L, float T4) {
+  const float a = (float)q.a, b = (float)q.b;
+  const float inv4s = 0.25f / fmaxf((float)q.s, 1e-30f);
+  float E = 0.0f;
+  for (int k = k0; k < L; ++k) {
+    float frac = 1.0f;
+    if (scs[k].invS != 0.0) {
+      const float h = a * (float)scs[k].B0 - b * (float)scs[k].A0;  // 2 sinh((r - c_k)/2)
+      const float ratio = (T4 - h * h) * inv4s * (float)scs[k].invS;
+      if (ratio < 1.0f) frac = 0.63661977f * asinf(sqrtf(fmaxf(ratio, 0.0f)));
+    }
+    E += (float)scs[k].nj * frac;
+  }
+  return E;
+}
+
+// item t < heavy_end: hub vertex t, work = its exact candidate count (lane k: slab k);
+// item heavy_end + g: light group g, work = sum of E(r) over its 32 vertices, scaled by
+// exact / E of its first vertex (which catches the lumpy angular distribution of the
+// few inner-slab points that every vertex of an arc sees).
+__global__ void __launch_bounds__(256)
+    k_shard_work(const QueryArgs A, const __grid_constant__ BandConst bc, int outward,
+                 uint32_t* __restrict__ work) {
+  __shared__ SlabC scs[kMaxBands];
+  __shared__ uint32_t start[kMaxBands + 1];
+  const int L = bc.L;
+  if (threadIdx.x < (unsigned)L) {
+    const int j = threadIdx.x;
+    SlabC c;
+    c.invS = bc.invS[j];
+    c.padS = bc.padS[j];
+    c.A0 = bc.A[j];
+    c.B0 = bc.B[j];
+    c.A1 = bc.A[j + 1];
+    c.B1 = bc.B[j + 1];
+    c.invS1 = bc.invS[j + 1];
+    c.start = A.lay->start[j];
+    c.nj = A.lay->start[j + 1] - c.start;
+    c.off = A.lay->dir_off[j];
+    c.sh = A.lay->shift[j];
+    scs[j] = c;
+  }
+  if (threadIdx.x <= (unsigned)L) start[threadIdx.x] = A.lay->start[threadIdx.x];
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t he = A.lay->heavy_end, nlight = A.n - he, ngroups = (nlight + 31u) / 32u;
+  const uint32_t items = he + ngroups, warps = gridDim.x * (blockDim.x >> 5);
+  const float T4f = (float)bc.T4;
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += warps) {
+    // representative vertex of the item (a hub, or the group's first vertex)
+    const uint32_t k0 = it < he ? it : A.order[(it - he) * 32u];
+    const uint32_t key0 = A.skey[k0], j0 = key0 >> kBandShift;
+    const PointRec q0 = A.pts[k0 + start[j0]];
+    const int kmin = outward ? (int)j0 : 0;
+    uint32_t c = 0;
+    if ((int)lane >= kmin && (int)lane < L)
+      c = slab_candidates(scs[lane], q0, key0, 0.25 / q0.s, bc, A.dir);
+    const float exact = (float)__reduce_add_sync(0xffffffffu, c);
+    float w;
+    if (it < he) {
+      w = exact;
+    } else {
+      const uint32_t idx = (it - he) * 32u + lane;
+      float e = 0.0f;
+      if (idx < nlight) {
+        const uint32_t k = A.order[idx];
+        const uint32_t key = A.skey[k], j = key >> kBandShift;
+        e = expected_candidates(A.pts[k + start[j]], scs, outward ? (int)j : 0, L, T4f);
+      }
+      const float e0 = __shfl_sync(0xffffffffu, e, 0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+      w = e0 > 0.0f ? e * (exact + 1.0f) / (e0 + 1.0f) : e;
+    }
+    if (lane == 0) work[it] = (uint32_t)fminf(ceilf(w) + 1.0f, 4.0e9f);
+  }
+}
+
+cudaError_t launch_shard_work(const QueryArgs& qa, const BandConst& bc, int outward, uint32_t* work,
+                              cudaStream_t st) {
+  k_shard_work<<<num_sms() * 8, 256, 0, st>>>(qa, bc, outward, work);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                               const BandConst& bc, void* scan_tmp, cudaStream_t st, int* launches) {
   uint32_t blocks = (uint32_t)((bc.heavy_cap + HV_WARPS - 1) / HV_WARPS);
@@ -1155,8 +1258,9 @@ cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
 
 cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const BandConst& bc,
                          cudaStream_t st) {
-  // warps for this shard's groups (upper bound: hubs are excluded on the device)
-  const uint32_t groups = ((qa.n + 31) / 32 + bc.nshards - 1) / bc.nshards + 1;
+  // one warp per light group (upper bound: hubs are excluded on the device; with
+  // shards the warps of other shards' groups exit at once)
+  const uint32_t groups = (qa.n + 31) / 32 + 1;
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
   // a slab may hold >= 2^30 points: 64-bit positions (or forced, rhg_options.wide_positions)

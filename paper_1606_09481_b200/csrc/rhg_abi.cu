@@ -126,7 +126,8 @@ struct Layout {
   size_t h_pstart, h_plen, h_poff, h_np, h_vtot, h_vtot_off, h_cc,
       h_choff, h_cvtx, h_cpiece, h_chits, h_cpos, h_meta, h_bits;
   size_t b_bits, b_over, q_order, q_cell_lo, q_cell_cnt, q_cell_off;
-  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps, dir_cap;
+  size_t s_work, s_prefix, s_plan, s_hub;
+  uint64_t vcap, nslots_cap, chunk_cap, hbits_cap, light_warps, dir_cap, item_cap;
 };
 
 constexpr uint64_t kChunkExtra = 1ull << 21;
@@ -150,6 +151,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   // per directed CSR entry); light warps get kLightBitRows x 32 words each.
   const uint64_t cap_tests = (f == RHG_CSR) ? cap + cap / 2 : 2 * cap;
   L.light_warps = (n + 31) / 32;
+  L.item_cap = L.vcap + L.light_warps + 1;  // shard plan: hub vertices + light groups
   L.hbits_cap = cap_tests / 32 + L.vcap * 48 + 1024;  // >= nchunks (CH/32 + 8) when hubs fit
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -178,6 +180,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
     if (L.vcap > m) m = L.vcap;
     if ((uint64_t)kQuerySectors * kMaxBands > m) m = (uint64_t)kQuerySectors * kMaxBands;
     if (L.chunk_cap > m) m = L.chunk_cap;
+    if (L.item_cap > m) m = L.item_cap;
     L.scan_tmp = take(scan_tmp_bytes(m));
     L.heavy_scan_tmp = take(scan_tmp_bytes(m));
   }
@@ -200,6 +203,10 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.q_cell_lo = take(4 * kQuerySectors * kMaxBands);
   L.q_cell_cnt = take(4 * kQuerySectors * kMaxBands);
   L.q_cell_off = take(8 * (kQuerySectors * kMaxBands + 1));
+  L.s_work = take(4 * L.item_cap);
+  L.s_prefix = take(8 * (L.item_cap + 1));
+  L.s_plan = take(sizeof(ShardPlan));
+  L.s_hub = take(8 * 4096);  // per-shard hub work (shard_count <= 4096)
   L.h_meta = take(sizeof(HeavyMeta));
   L.sc = take(sizeof(DevScalars));
   L.st_rowptr = host && f == RHG_CSR ? take(8 * (n + 1)) : o;
@@ -460,7 +467,14 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa.deg = deg;
   qa.cdeg = (uint32_t*)(ws + Lw.cdeg);
   qa.sc = sc;
-  if (bc.nshards > 1) CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of other shards stay empty
+  if (bc.nshards > 1) {
+    CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of other shards stay empty
+    qa.shard_plan = (const ShardPlan*)(ws + Lw.s_plan);
+    CK(launch_shard_plan((uint32_t)n, qa, bc, f == RHG_EDGES_UNDIRECTED ? 1 : 0,
+                         (uint32_t*)(ws + Lw.s_work), (uint64_t*)(ws + Lw.s_prefix), Lw.item_cap,
+                         ws + Lw.scan_tmp, (unsigned long long*)(ws + Lw.s_hub),
+                         (ShardPlan*)(ws + Lw.s_plan), st, &launches));
+  }
   ha = HeavyArgs{};
   ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
   ha.plen = (uint32_t*)(ws + Lw.h_plen);

@@ -106,8 +106,21 @@ struct __align__(16) PointRec {
   double theta, s, a, b;
 };
 
+// Sharding (k_shard.cu): hub vertex i belongs to shard snake(i); the
+// light groups [grp_beg, grp_end) of the sector-major order to this shard.
+struct ShardPlan {
+  uint32_t grp_beg, grp_end;      // this shard's light groups
+  unsigned long long work_total;  // estimated candidates of all query items
+  unsigned long long hub_work;    // estimated candidates of this shard's hubs
+};
+__host__ __device__ __forceinline__ uint32_t snake(uint64_t c, uint32_t N) {
+  const uint32_t m = (uint32_t)(c % (2ull * N));
+  return m < N ? m : 2u * N - 1u - m;
+}
+
 struct QueryArgs {
   uint32_t n;
+  const ShardPlan* shard_plan;        // nshards > 1: this shard's items (k_shard.cu), else null
   const PointRec* __restrict__ pts;   // doubled SoA: slab j at [2 start_j, 2 start_j + 2 n_j), two copies
   const uint32_t* __restrict__ skey;  // sorted keys [n]
   const uint32_t* __restrict__ sid;   // sorted position -> vertex id [n]
@@ -130,11 +143,6 @@ struct QueryArgs {
   const unsigned long long* total_dev;  // emit: skip everything if *total_dev > cap
   unsigned long long cap;
 };
-
-// Shard s of N owns items [floor(T s / N), floor(T (s+1) / N)) of a list of T.
-__host__ __device__ __forceinline__ uint64_t shard_begin(uint64_t T, uint32_t s, uint32_t N) {
-  return T * s / N;
-}
 
 // ---- K1 device code shared by the sampler and the generate-path gather ----
 // Philox4x32-10 (Salmon et al. 2011): counter (i_lo, i_hi, 0, 0), key = seed.
@@ -230,6 +238,16 @@ cudaError_t launch_heavy_plan(rhg_format fmt, const QueryArgs& qa, const HeavyAr
                               const BandConst& bc, void* scan_tmp, cudaStream_t st, int* launches);
 cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const HeavyArgs& ha,
                          const BandConst& bc, cudaStream_t st);
+
+// Shard plan (k_shard.cu): estimated work per query item (launch_shard_work, in
+// k_query.cu), its scan, the hubs' work per shard and this shard's light range.
+// work / prefix hold item_cap (+1) entries, item_cap >= heavy_end + ceil(light / 32).
+cudaError_t launch_shard_work(const QueryArgs& qa, const BandConst& bc, int outward, uint32_t* work,
+                              cudaStream_t st);
+cudaError_t launch_shard_plan(uint32_t n, const QueryArgs& qa, const BandConst& bc, int outward,
+                              uint32_t* work, uint64_t* prefix, uint64_t item_cap, void* scan_tmp,
+                              unsigned long long* hub_work, ShardPlan* plan, cudaStream_t st,
+                              int* launches);
 
 // Validation statistics (k_stats.cu)
 size_t stats_workspace_bytes(uint64_t n);

@@ -681,3 +681,28 @@ def test_graph_mode_host_buffers(rhg):
             s.synchronize()
             assert g.num_edges == ref.num_edges
             assert torch.equal(rp, ref.row_ptr.cpu()) and torch.equal(col, ref.col.cpu())
+
+
+@pytest.mark.parametrize("fmt", ["csr", "pairs"])
+def test_shard_work_balance(rhg, fmt):
+    """shards take equal shares of the work (light groups in interleaved
+    blocks, hubs dealt in snake order; rhg_internal.cuh).  At config 4 (gamma = 2.2,
+    hubs carry ~25 % of the tests) the candidates each shard visits (tests +
+    certain) are within 5 % of the mean for N = 2, 3 and 8, and the shards still
+    partition the graph."""
+    n, kbar, gamma, seed = CONFIGS[4]
+    full = rhg.generate(n, kbar, gamma, seed, fmt, timing=True)
+    tot = full.timing["candidates"] + full.timing["certain"]
+    for N in (2, 3, 8):
+        work, edges = [], 0
+        for s in range(N):
+            g = rhg.generate(n, kbar, gamma, seed, fmt, timing=True,
+                             options=dict(shard_index=s, shard_count=N))
+            work.append(g.timing["candidates"] + g.timing["certain"])
+            edges += g.num_edges
+        assert edges == full.num_edges
+        assert sum(work) == tot
+        mean = tot / N
+        dev = max(abs(w - mean) for w in work) / mean
+        print(f"{fmt} N={N}: per-shard candidates {work}, max deviation {dev:.3%}")
+        assert dev <= 0.05, (N, work)
