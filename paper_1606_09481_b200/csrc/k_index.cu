@@ -3,6 +3,7 @@
 // PAPER.md:214 ("find the leftmost and rightmost neighbor candidate in each slab
 // using binary search").
 #include "rhg_internal.cuh"
+#include "rhg_predicate.cuh"
 
 namespace rhg {
 
@@ -16,26 +17,9 @@ __device__ __forceinline__ uint32_t warp_incl_u32(uint32_t v) {
   return v;
 }
 
-// Point record for sorted position k: theta, sinh r, e^{r/2}, e^{-r/2}.
-// (cosh d - 1 = 2 sinh^2((r_p - r_q)/2) + 2 sinh r_p sinh r_q sin^2(dphi/2), and
-//  2 sinh((r_p - r_q)/2) = e^{r_p/2} e^{-r_q/2} - e^{-r_p/2} e^{r_q/2}.)
 // Doubled SoA: the record of sorted position k in slab j (start s_j, n_j points)
 // is written at k + s_j and k + s_j + n_j, so slab j occupies [2 s_j, 2 s_j + 2 n_j)
 // as two back-to-back copies and every arc across 2 pi is one index range.
-// The query record of one point: e^{r/2} from exp, e^{-r/2} as its correctly
-// rounded reciprocal, and sinh r = (e^{r/2} - e^{-r/2})(e^{r/2} + e^{-r/2}) / 2 for
-// r >= 1 (no cancellation there: the first factor is >= 2 sinh(1/2)), sinh() below.
-// A few ulp from libm's values at most -- far inside the near-tie window the edge
-// predicate is checked against; both endpoints of a pair read the same record.
-__device__ __forceinline__ PointRec point_rec(double th, double rr) {
-  PointRec p;
-  p.theta = th;
-  p.a = exp(0.5 * rr);
-  p.b = __drcp_rn(p.a);
-  p.s = rr >= 1.0 ? 0.5 * ((p.a - p.b) * (p.a + p.b)) : sinh(rr);
-  return p;
-}
-
 __device__ __forceinline__ void put_doubled(uint32_t k, uint32_t key, const BandLayout* lay,
                                             const PointRec& p, uint32_t id,
                                             PointRec* __restrict__ pts, uint32_t* __restrict__ sid2) {
