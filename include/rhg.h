@@ -222,6 +222,48 @@ rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint64_t *row_pt
                            void *workspace, size_t workspace_bytes, rhg_stats *out,
                            rhg_stream stream);
 
+/* ---- Dynamic model: incremental edge update ----
+   PAPER.md:387-389 (§4): "Our implementation allows updating a graph without
+   rebuilding it from scratch.  Moving up to 12% of nodes and updating an existing
+   graph is still faster than a new static generation."  (Movement: rhg_move_points,
+   PAPER.md:223-254.)
+   Inputs (device pointers): the NEW positions theta[n], r[n] of all points (domain as
+   in rhg_generate_from_points); moved[m]: the ids of the vertices whose position
+   changed (distinct, < n); theta_old[m], r_old[m]: their OLD positions (same order);
+   old_row_ptr[n+1], old_col: the graph of the old positions as a CSR over vertex ids
+   (both directions), e.g. rhg_generate_from_points' output with vertex_order 0.
+   Output: the undirected edges (u < v) to remove from and to add to the old graph so
+   that it becomes the graph of the new positions (each list deterministic, order
+   unspecified).  The new points are indexed once (band assignment, sort, SoA,
+   directory), the range queries of Alg. 1 run for the moved vertices only, and each
+   moved vertex's old and new rows are compared with the certified test of Eq. 3.
+   Errors: RHG_ERR_INVALID (arguments), RHG_ERR_DOMAIN (a new point outside the disk),
+   RHG_ERR_WORKSPACE (workspace smaller than rhg_update_workspace_bytes(n, row_capacity)
+   or the moved vertices' new rows need more than row_capacity entries; the required
+   number is written to *rows_needed when given), RHG_ERR_CAPACITY (added or removed
+   exceeds capacity; both counts are written, nothing else), RHG_ERR_CUDA.
+   Synchronises `stream` twice (row total, delta totals). */
+typedef struct {
+  uint32_t *added;         /* device, 2*capacity entries: (u, v) pairs, u < v                */
+  uint32_t *removed;       /* device, 2*capacity entries                                    */
+  uint64_t capacity;       /* pairs each list can hold                                      */
+  uint64_t *num_added;     /* HOST, required                                                */
+  uint64_t *num_removed;   /* HOST, required                                                */
+  uint64_t row_capacity;   /* directed entries the moved vertices' new rows may take        */
+  uint64_t *rows_needed;   /* HOST, optional: the entries the new rows took / need          */
+  void *workspace;         /* device scratch, >= rhg_update_workspace_bytes(n, row_capacity) */
+  size_t workspace_bytes;
+  const rhg_options *options; /* slab layout knobs (num_bands, band_ratio); NULL: defaults  */
+  rhg_timing *timing;      /* HOST, optional: ms_sort, ms_index, ms_count, ms_emit (rows +
+                              delta), ms_total, candidates, certain                        */
+} rhg_update;
+
+size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity, const rhg_options *options);
+rhg_status rhg_update_moved(uint64_t n, const double *theta, const double *r, double R,
+                            const uint32_t *moved, uint64_t m, const double *theta_old,
+                            const double *r_old, const uint64_t *old_row_ptr,
+                            const uint32_t *old_col, const rhg_update *out, rhg_stream stream);
+
 /* Edges of a given point set (Alg. 1 lines 9-21): theta[n] in [0, 2pi),
    r[n] in [0, R], fp64, device pointers (host if out->host_buffers).  Ids are
    the input indices.  Out-of-domain points -> RHG_ERR_DOMAIN. */

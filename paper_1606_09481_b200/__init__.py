@@ -32,7 +32,8 @@ ABI_SYMBOLS = ("rhg_target_radius", "rhg_band_boundaries", "rhg_workspace_bytes"
                "rhg_generate_with_radius", "rhg_generate_from_points", "rhg_sample_points",
                "rhg_philox_words", "rhg_status_string", "rhg_version", "rhg_last_cuda_error",
                "rhg_generate_with_C", "rhg_movement_init", "rhg_move_points",
-               "rhg_stats_workspace_bytes", "rhg_graph_stats")
+               "rhg_stats_workspace_bytes", "rhg_graph_stats", "rhg_update_workspace_bytes",
+               "rhg_update_moved")
 STATS_BINS = 40
 
 
@@ -72,6 +73,15 @@ class Stats(ctypes.Structure):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "degree_hist"}
         d["degree_hist"] = list(self.degree_hist)
         return d
+
+
+class Update(ctypes.Structure):
+    _fields_ = [("added", ctypes.c_void_p), ("removed", ctypes.c_void_p),
+                ("capacity", ctypes.c_uint64), ("num_added", ctypes.POINTER(ctypes.c_uint64)),
+                ("num_removed", ctypes.POINTER(ctypes.c_uint64)), ("row_capacity", ctypes.c_uint64),
+                ("rows_needed", ctypes.POINTER(ctypes.c_uint64)), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("options", ctypes.c_void_p),
+                ("timing", ctypes.c_void_p)]
 
 
 class Output(ctypes.Structure):
@@ -116,6 +126,11 @@ def lib() -> ctypes.CDLL:
         L.rhg_sample_points.argtypes = [u64, f64, f64, u64, vp, vp, vp]
         L.rhg_philox_words.restype = st
         L.rhg_philox_words.argtypes = [u64, u64, u64, vp, vp]
+        L.rhg_update_workspace_bytes.restype = ctypes.c_size_t
+        L.rhg_update_workspace_bytes.argtypes = [u64, u64, ctypes.POINTER(Options)]
+        L.rhg_update_moved.restype = st
+        L.rhg_update_moved.argtypes = [u64, vp, vp, f64, vp, u64, vp, vp, vp, vp,
+                                       ctypes.POINTER(Update), vp]
         L.rhg_status_string.restype = ctypes.c_char_p
         L.rhg_status_string.argtypes = [ctypes.c_int]
         L.rhg_version.restype = ctypes.c_char_p
@@ -420,6 +435,59 @@ def generate_from_points(theta, r, R: float, fmt: str = "csr", *, capacity=None,
                 n, fmt, hint, device=device, capacity=capacity, options=options, timing=timing,
                 workspace=workspace, stream=stream, host_buffers=host, want_points=False,
                 sample=False)
+
+
+@dataclass
+class Delta:
+    added: object      # torch int32 [num_added, 2], u < v
+    removed: object    # torch int32 [num_removed, 2], u < v
+    rows: int          # directed entries of the moved vertices' new rows
+    timing: dict = field(default_factory=dict)
+
+
+def update_moved(theta, r, R: float, moved, theta_old, r_old, old_row_ptr, old_col, *,
+                 options=None, timing=False, workspace=None, stream=None, capacity=None,
+                 row_capacity=None) -> Delta:
+    """Edge delta of the dynamic model (rhg_update_moved): the new
+    positions of all points, the moved vertex ids (int32, distinct) with their old
+    positions, and the old graph's CSR (CUDA tensors).  Sizes its buffers from the
+    library's required counts (one retry at most per buffer)."""
+    torch = _torch()
+    for t in (theta, r, theta_old, r_old):
+        assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+    n, m = theta.numel(), moved.numel()
+    dev = theta.device
+    L = lib()
+    opts = _options(options)
+    old_deg = torch.diff(old_row_ptr)[moved.long()] if m else torch.zeros(1, device=dev)
+    rcap = int(row_capacity) if row_capacity is not None else int(2 * old_deg.sum().item()) + 64 * m + 4096
+    cap = int(capacity) if capacity is not None else rcap // 2 + 4096
+    ws = workspace if workspace is not None else Workspace(dev)
+    tm = Timing()
+    for _ in range(3):
+        wb = ws.get(int(L.rhg_update_workspace_bytes(n, rcap, ctypes.byref(opts))))
+        added = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
+        removed = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
+        na, nr, rn = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        u = Update(added.data_ptr(), removed.data_ptr(), cap, ctypes.pointer(na), ctypes.pointer(nr),
+                   rcap, ctypes.pointer(rn), wb.data_ptr(), wb.numel(),
+                   ctypes.cast(ctypes.pointer(opts), ctypes.c_void_p),
+                   ctypes.cast(ctypes.pointer(tm), ctypes.c_void_p) if timing else None)
+        st = L.rhg_update_moved(n, theta.data_ptr(), r.data_ptr(), R, moved.data_ptr() if m else None,
+                                m, theta_old.data_ptr() if m else None,
+                                r_old.data_ptr() if m else None, old_row_ptr.data_ptr(),
+                                old_col.data_ptr() if old_col.numel() else None, ctypes.byref(u),
+                                _stream_handle(stream))
+        if st == RHG_ERR_WORKSPACE and rn.value > rcap:
+            rcap = int(rn.value)
+            continue
+        if st == RHG_ERR_CAPACITY:
+            cap = int(max(na.value, nr.value))
+            continue
+        _check(st)
+        return Delta(added=added[: na.value], removed=removed[: nr.value], rows=int(rn.value),
+                     timing=tm.as_dict() if timing else {})
+    raise RuntimeError("rhg_update_moved: buffers could not be sized")
 
 
 def sample_points(n: int, alpha: float, R: float, seed: int, device="cuda", stream=None):

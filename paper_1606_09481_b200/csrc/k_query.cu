@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t g = blockIdx.x * QK_WARPS + (threadIdx.x >> 5);  // light warp (of this shard)
-  const uint32_t nlight = A.n - A.lay->heavy_end;
+  const uint32_t nlight = A.nquery ? (uint32_t)*A.nquery : A.n - A.lay->heavy_end;
   // shard: a contiguous range of the 32-vertex groups of the sector-major order
   // with an equal share of the estimated work (k_shard.cu)
   const uint32_t ngroups = (nlight + 31u) / 32u;
@@ -838,7 +838,8 @@ __global__ void __launch_bounds__(HV_THREADS)
     const uint32_t qband = qkey >> kBandShift;
     const PointRec q = A.pts[i + bs.start[qband]];
     const double qinv4s = 0.25 / q.s;
-    const bool owned = bc.nshards <= 1 || snake(i, bc.nshards) == bc.shard;
+    const bool owned = (bc.nshards <= 1 || snake(i, bc.nshards) == bc.shard) &&
+                       (!A.hub_mask || A.hub_mask[i] != 0u);
     const int j = owned ? lane : 32;  // other shards' hubs: no pieces
     int64_t lo[6] = {0, 0, 0, 0, 0, 0}, ln[6] = {0, 0, 0, 0, 0, 0};
     uint32_t gbase = 0;
@@ -1190,9 +1191,9 @@ cudaError_t launch_heavy(QueryMode mode, rhg_format fmt, const QueryArgs& qa, co
 
 cudaError_t launch_query(QueryMode mode, rhg_format fmt, const QueryArgs& qa, const BandConst& bc,
                          cudaStream_t st) {
-  // one warp per light group (upper bound: hubs are excluded on the device; with
-  // shards the warps of other shards' groups exit at once)
-  const uint32_t groups = (qa.n + 31) / 32 + 1;
+  // one warp per light group (upper bound: hubs are excluded and a shard's range is
+  // known on the device only)
+  const uint32_t groups = ((qa.nquery_max ? qa.nquery_max : qa.n) + 31) / 32 + 1;
   const uint32_t blocks = (groups + QK_WARPS - 1) / QK_WARPS;
   if (blocks == 0) return cudaSuccess;
   // a slab may hold >= 2^30 points: 64-bit positions (or forced, rhg_options.wide_positions)

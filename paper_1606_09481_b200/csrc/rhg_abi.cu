@@ -637,6 +637,200 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   return RHG_OK;
 }
 
+// ------------------------------------------------------------------ dynamic update
+// Workspace of rhg_update_moved: the generator's layout (no hub scratch, no output
+// staging) plus the update's arrays.
+struct UpdLayout {
+  Layout base;
+  size_t midx, flag, fpos, qorder, nlm, new_col, n_rem, n_add, off_rem, off_add, total;
+};
+
+UpdLayout plan_update(uint64_t n, uint64_t row_capacity, int nbands) {
+  UpdLayout U{};
+  U.base = plan_layout(n, RHG_CSR, 0, 0, nbands);
+  size_t o = U.base.total;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  U.midx = take(4 * n);
+  U.flag = take(4 * n);
+  U.fpos = take(8 * (n + 1));
+  U.qorder = take(4 * n);
+  U.nlm = take(8);
+  U.new_col = take(4 * (row_capacity ? row_capacity : 1));
+  U.n_rem = take(4 * n);
+  U.n_add = take(4 * n);
+  U.off_rem = take(8 * (n + 1));
+  U.off_add = take(8 * (n + 1));
+  U.total = o;
+  return U;
+}
+
+// SURVEY §8(f) f1 (k_update.cu): index the new points, query the moved vertices'
+// new rows (count -> scan -> emit, as in run()), compare them with the old rows.
+rhg_status run_update(uint64_t n, const double* theta, const double* r, double R,
+                      const uint32_t* moved, uint64_t m, const double* theta_old,
+                      const double* r_old, const uint64_t* old_rp, const uint32_t* old_col,
+                      const rhg_update* out, cudaStream_t st) {
+  if (!out || !out->num_added || !out->num_removed) return RHG_ERR_INVALID;
+  if (n < 2 || n >= (1ull << 31) || m > n) return RHG_ERR_INVALID;
+  if (!theta || !r || !old_rp || (m && (!moved || !theta_old || !r_old))) return RHG_ERR_INVALID;
+  if (!(R >= 0.0) || !std::isfinite(R) || !std::isfinite(std::sinh(R / 2.0) * std::sinh(R / 2.0) * 4.0))
+    return RHG_ERR_INVALID;
+  if (out->capacity && (!out->added || !out->removed)) return RHG_ERR_INVALID;
+  rhg_options opt{};
+  if (out->options) {
+    opt.num_bands = out->options->num_bands;
+    opt.band_ratio = out->options->band_ratio;
+    opt.heavy_threshold = out->options->heavy_threshold;
+  }
+  BandConst bc;
+  rhg_status s = make_band_const(n, R, &opt, &bc);
+  if (s != RHG_OK) return s;
+  const UpdLayout U = plan_update(n, out->row_capacity, bc.L);
+  const Layout& Lw = U.base;
+  if (!out->workspace || out->workspace_bytes < U.total) return RHG_ERR_WORKSPACE;
+  DevScalars* pin = pinned_scalars();
+  if (!pin) return RHG_ERR_CUDA;
+  char* ws = (char*)out->workspace;
+  uint32_t* keys_a = (uint32_t*)(ws + Lw.keys_a);
+  uint32_t* vals_a = (uint32_t*)(ws + Lw.vals_a);
+  uint32_t* hist = (uint32_t*)(ws + Lw.hist);
+  BandLayout* lay = (BandLayout*)(ws + Lw.lay);
+  PointRec* pts = (PointRec*)(ws + Lw.pts);
+  uint32_t* sid2 = (uint32_t*)(ws + Lw.sid2);
+  uint32_t* dir = (uint32_t*)(ws + Lw.dir);
+  uint32_t* deg = (uint32_t*)(ws + Lw.deg);
+  uint64_t* offs = (uint64_t*)(ws + Lw.offs);
+  DevScalars* sc = (DevScalars*)(ws + Lw.sc);
+  uint64_t* fpos = (uint64_t*)(ws + U.fpos);
+  uint32_t* new_col = (uint32_t*)(ws + U.new_col);
+  Timer tm;
+  tm.init(out->timing != nullptr, st);
+  int launches = 0;
+  CK(radix_sort_prepare());
+  tm.mark();  // 0
+  CK(cudaMemsetAsync(hist, 0, 4 * kMaxBands, st));
+  CK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), st));
+  CK(launch_keys_from_points(n, theta, r, bc, keys_a, vals_a, hist, sc, st));
+  CK(launch_band_layout(bc, hist, lay, (HeavyMeta*)(ws + Lw.h_meta), st));
+  CK(radix_sort((uint32_t)n, keys_a, vals_a, (uint32_t*)(ws + Lw.keys_b), (uint32_t*)(ws + Lw.vals_b),
+                ws + Lw.sort_tmp, 0, 32, st, &launches));
+  tm.mark();  // 1
+  CK(launch_build_index((uint32_t)n, theta, r, keys_a, vals_a, lay, bc.L, pts, sid2, dir, nullptr, 0,
+                        st, &launches));
+  CK(launch_query_order(keys_a, lay, bc.L, (uint32_t*)(ws + Lw.q_cell_lo),
+                        (uint32_t*)(ws + Lw.q_cell_cnt), (uint64_t*)(ws + Lw.q_cell_off),
+                        (uint32_t*)(ws + Lw.q_order), ws + Lw.scan_tmp, st, &launches));
+  // the moved vertices' sorted positions in processing order (hubs included: the
+  // light kernel handles any vertex)
+  CK(launch_update_select((uint32_t)n, m, moved, lay, (const uint32_t*)(ws + Lw.q_order), vals_a,
+                          (uint32_t*)(ws + U.midx), (uint32_t*)(ws + U.flag), fpos,
+                          (uint32_t*)(ws + U.qorder), (unsigned long long*)(ws + U.nlm),
+                          ws + Lw.scan_tmp, st, &launches));
+  tm.mark();  // 2
+  QueryArgs qa{};
+  qa.n = (uint32_t)n;
+  qa.nquery = (const unsigned long long*)(ws + U.nlm);
+  qa.nquery_max = (uint32_t)m;
+  qa.hub_mask = (const uint32_t*)(ws + U.flag);  // items [0, heavy_end) = hub positions
+  qa.stats = out->timing ? 1u : 0u;
+  qa.pts = pts;
+  qa.skey = keys_a;
+  qa.sid = vals_a;
+  qa.sid2 = sid2;
+  qa.dir = dir;
+  qa.lay = lay;
+  qa.order = (const uint32_t*)(ws + U.qorder);
+  qa.bits = (uint32_t*)(ws + Lw.b_bits);
+  qa.warp_over = (uint32_t*)(ws + Lw.b_over);
+  qa.deg = deg;
+  qa.cdeg = (uint32_t*)(ws + Lw.cdeg);
+  qa.sc = sc;
+  CK(cudaMemsetAsync(deg, 0, 4 * n, st));  // rows of vertices that did not move stay empty
+  HeavyMeta* hmeta = (HeavyMeta*)(ws + Lw.h_meta);
+  HeavyArgs ha{};
+  ha.pstart = (uint32_t*)(ws + Lw.h_pstart);
+  ha.plen = (uint32_t*)(ws + Lw.h_plen);
+  ha.poff = (uint32_t*)(ws + Lw.h_poff);
+  ha.np = (uint32_t*)(ws + Lw.h_np);
+  ha.vtot = (uint32_t*)(ws + Lw.h_vtot);
+  ha.vtot_off = (uint64_t*)(ws + Lw.h_vtot_off);
+  ha.cc = (uint32_t*)(ws + Lw.h_cc);
+  ha.choff = (uint64_t*)(ws + Lw.h_choff);
+  ha.chunk_vtx = (uint32_t*)(ws + Lw.h_cvtx);
+  ha.chunk_piece = (uint32_t*)(ws + Lw.h_cpiece);
+  ha.chunk_hits = (uint32_t*)(ws + Lw.h_chits);
+  ha.chunk_pos = (uint64_t*)(ws + Lw.h_cpos);
+  ha.bits = (uint32_t*)(ws + Lw.h_bits);
+  ha.bits_cap = Lw.hbits_cap;
+  ha.meta = hmeta;
+  ha.vcap = Lw.vcap;
+  ha.chunk_cap = Lw.chunk_cap;
+  ha.chunk_min = kChunkMin;
+  if (m) {
+    // moved hubs: the chunked hub path (hub_mask), the rest: light warps
+    CK(launch_heavy_plan(RHG_CSR, qa, ha, bc, ws + Lw.heavy_scan_tmp, st, &launches));
+    CK(launch_heavy(QM_COUNT, RHG_CSR, qa, ha, bc, st));
+    CK(exclusive_scan_u32_u64_dev(ha.chunk_cap, &hmeta->nchunks, ha.chunk_hits, ha.chunk_pos,
+                                  ws + Lw.heavy_scan_tmp, &hmeta->hits, st, &launches));
+    CK(launch_query(QM_COUNT, RHG_CSR, qa, bc, st));
+  }
+  CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
+  tm.mark();  // 3
+  CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const DevScalars hs = *pin;
+  if (hs.domain_error) return RHG_ERR_DOMAIN;
+  if (out->rows_needed) *out->rows_needed = hs.total;
+  if (hs.total > out->row_capacity) return RHG_ERR_WORKSPACE;
+  qa.offs = offs;
+  qa.col = new_col;
+  qa.out_cap = out->row_capacity;
+  if (m) {
+    CK(launch_heavy(QM_EMIT_BITS, RHG_CSR, qa, ha, bc, st));
+    CK(launch_query(QM_EMIT_BITS, RHG_CSR, qa, bc, st));
+  }
+  uint32_t* n_rem = (uint32_t*)(ws + U.n_rem);
+  uint32_t* n_add = (uint32_t*)(ws + U.n_add);
+  uint64_t* off_rem = (uint64_t*)(ws + U.off_rem);
+  uint64_t* off_add = (uint64_t*)(ws + U.off_add);
+  const uint32_t* midx = (const uint32_t*)(ws + U.midx);
+  CK(launch_delta(false, m, moved, midx, theta, r, theta_old, r_old, old_rp, old_col, offs, new_col,
+                  bc.T4, n_rem, n_add, nullptr, nullptr, nullptr, nullptr, st));
+  CK(exclusive_scan_u32_u64((uint32_t)(m ? m : 1), n_rem, off_rem, ws + Lw.scan_tmp, &sc->candidates,
+                            st, &launches));
+  CK(exclusive_scan_u32_u64((uint32_t)(m ? m : 1), n_add, off_add, ws + Lw.scan_tmp, &sc->certain,
+                            st, &launches));
+  CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint64_t nrem = m ? pin->candidates : 0, nadd = m ? pin->certain : 0;
+  *out->num_removed = nrem;
+  *out->num_added = nadd;
+  if (nrem > out->capacity || nadd > out->capacity) return RHG_ERR_CAPACITY;
+  CK(launch_delta(true, m, moved, midx, theta, r, theta_old, r_old, old_rp, old_col, offs, new_col,
+                  bc.T4, n_rem, n_add, off_rem, off_add, out->removed, out->added, st));
+  tm.mark();  // 4
+  if (out->timing) {
+    CK(cudaStreamSynchronize(st));
+    rhg_timing* t = out->timing;
+    memset(t, 0, sizeof(*t));
+    t->ms_sort = tm.between(0, 1);
+    t->ms_index = tm.between(1, 2);
+    t->ms_count = tm.between(2, 3);
+    t->ms_emit = tm.between(3, 4);
+    t->ms_total = tm.between(0, 4);
+    t->candidates = hs.candidates;
+    t->certain = hs.certain;
+    t->launches = (uint64_t)launches;
+    t->emit_retested = hs.bit_overflow;
+  }
+  CK(cudaGetLastError());
+  return RHG_OK;
+}
+
 }  // namespace
 
 namespace rhg {
@@ -738,6 +932,20 @@ RHG_EXPORT rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint6
   CK(launch_graph_stats((uint32_t)n, format, row_ptr, col, pairs, m, theta, r, R, k_min, workspace,
                         out, (cudaStream_t)stream));
   return RHG_OK;
+}
+
+RHG_EXPORT size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity,
+                                             const rhg_options* options) {
+  return plan_update(n, row_capacity, bands_for(n, options)).total;
+}
+
+RHG_EXPORT rhg_status rhg_update_moved(uint64_t n, const double* theta, const double* r, double R,
+                                       const uint32_t* moved, uint64_t m, const double* theta_old,
+                                       const double* r_old, const uint64_t* old_row_ptr,
+                                       const uint32_t* old_col, const rhg_update* out,
+                                       rhg_stream stream) {
+  return run_update(n, theta, r, R, moved, m, theta_old, r_old, old_row_ptr, old_col, out,
+                    (cudaStream_t)stream);
 }
 
 RHG_EXPORT rhg_status rhg_generate_from_points(uint64_t n, const double* theta, const double* r, double R,

@@ -120,6 +120,9 @@ __host__ __device__ __forceinline__ uint32_t snake(uint64_t c, uint32_t N) {
 
 struct QueryArgs {
   uint32_t n;
+  const unsigned long long* nquery;   // device: light query items in `order` (null: n - heavy_end)
+  uint32_t nquery_max;                // host bound of *nquery for the grid (0: n)
+  const uint32_t* hub_mask;           // non-null: only hubs i with hub_mask[i] != 0 are queried
   const ShardPlan* shard_plan;        // nshards > 1: this shard's items (k_shard.cu), else null
   const PointRec* __restrict__ pts;   // doubled SoA: slab j at [2 start_j, 2 start_j + 2 n_j), two copies
   const uint32_t* __restrict__ skey;  // sorted keys [n]
@@ -248,6 +251,21 @@ cudaError_t launch_shard_plan(uint32_t n, const QueryArgs& qa, const BandConst& 
                               uint32_t* work, uint64_t* prefix, uint64_t item_cap, void* scan_tmp,
                               unsigned long long* hub_work, ShardPlan* plan, cudaStream_t st,
                               int* launches);
+
+// Incremental update of the dynamic model (k_update.cu)
+// flag[t] = 1 if query item t (hub position t < heavy_end, else light order entry)
+// moved; qorder = the moved light entries in processing order, *nlight_moved their count
+cudaError_t launch_update_select(uint32_t n, uint64_t m, const uint32_t* moved, const BandLayout* lay,
+                                 const uint32_t* order, const uint32_t* sid, uint32_t* midx,
+                                 uint32_t* flag, uint64_t* fpos, uint32_t* qorder,
+                                 unsigned long long* nlight_moved, void* scan_tmp, cudaStream_t st,
+                                 int* launches);
+cudaError_t launch_delta(bool write, uint64_t m, const uint32_t* moved, const uint32_t* midx,
+                         const double* theta, const double* r, const double* theta_old,
+                         const double* r_old, const uint64_t* old_rp, const uint32_t* old_col,
+                         const uint64_t* new_rp, const uint32_t* new_col, double T4, uint32_t* n_rem,
+                         uint32_t* n_add, const uint64_t* off_rem, const uint64_t* off_add,
+                         uint32_t* removed, uint32_t* added, cudaStream_t st);
 
 // Validation statistics (k_stats.cu)
 size_t stats_workspace_bytes(uint64_t n);

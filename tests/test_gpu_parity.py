@@ -706,3 +706,42 @@ def test_shard_work_balance(rhg, fmt):
         dev = max(abs(w - mean) for w in work) / mean
         print(f"{fmt} N={N}: per-shard candidates {work}, max deviation {dev:.3%}")
         assert dev <= 0.05, (N, work)
+
+
+# --------------------------------------------------------------------------- f1 update
+@pytest.mark.parametrize("frac", [0.01, 0.05, 0.12])
+def test_update_moved_matches_oracle(rhg, orc, frac):
+    """move a subset of the vertices with the
+    dynamic model (rotation + Alg. 2, the oracle's step), update the GPU graph of the
+    old positions with rhg_update_moved, and compare old - removed + added with the
+    oracle's edge set of the new positions (exact except flagged near ties).  The
+    moved set includes the innermost vertices (hubs: the chunked path)."""
+    n, kbar, gamma, seed = 200_000, 12, 2.4, 41
+    th, r, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    g0 = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R, "csr")
+    tp, tr = orc.movement_init(n, 5)
+    th1, r1, _ = orc.move_points(th, r, tp, tr, R, a)
+    rng = np.random.default_rng(int(frac * 1000))
+    ids = np.unique(np.concatenate([rng.choice(n, int(frac * n), replace=False),
+                                    np.argsort(r)[:20]])).astype(np.int64)
+    th_new, r_new = th.copy(), r.copy()
+    th_new[ids], r_new[ids] = th1[ids], r1[ids]
+    d = rhg.update_moved(torch.from_numpy(th_new).cuda(), torch.from_numpy(r_new).cuda(), R,
+                         torch.from_numpy(ids.astype(np.int32)).cuda(),
+                         torch.from_numpy(th[ids]).cuda(), torch.from_numpy(r[ids]).cuda(),
+                         g0.row_ptr, g0.col)
+    old = csr_checked_pairs(g0)
+    rem = pairs_checked(rhg.Graph(n=n, format="pairs", R=R, num_edges=len(d.removed), pairs=d.removed))
+    add = pairs_checked(rhg.Graph(n=n, format="pairs", R=R, num_edges=len(d.added), pairs=d.added))
+    assert len(np.setdiff1d(rem, old)) == 0, "removed an edge that was not there"
+    assert len(np.intersect1d(add, old)) == 0, "added an edge that was already there"
+    new = np.union1d(np.setdiff1d(old, rem, assume_unique=True), add)
+    es = orc.sweep(th_new, r_new, R)
+    excused = compare_sets(new, es)
+    # nothing changes for pairs of two static vertices: every delta pair touches a moved one
+    mv = np.zeros(n, dtype=bool)
+    mv[ids] = True
+    for k in (rem, add):
+        u, v = (k >> np.uint64(32)).astype(np.int64), (k & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        assert np.all(mv[u] | mv[v])
+    print(f"moved {len(ids)} ({frac:.0%}): removed {len(rem)} added {len(add)} excused {excused}")
