@@ -433,8 +433,11 @@ def run_ours(args):
         e2e = measure_e2e(rhg, torch, c, seed, dev, ws, cap, args, opts)
         e2e["from_points"] = measure_e2e_points(rhg, torch, c, seed, dev, ws, cap, args, opts)
     near = None
+    dyn = None
     if rank == 0 and world == 1:
         near = near_tie_stats(rhg, torch, c, seed, dev, opts)
+        if not args.no_dynamic:
+            dyn = dynamic_update(rhg, torch, c, seed, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         oracle.build()
@@ -469,7 +472,7 @@ def run_ours(args):
                 "roofline": dominant, "roofline_other": roof_emit if dominant is roof_count else roof_count,
                 "north_star_hbm": north_star, "issue_rate": issue,
                 "phases_ms": ph, "candidates": cand, "other_vertex_order": other_line,
-                "configs_1gpu": configs, "near_ties": near,
+                "configs_1gpu": configs, "near_ties": near, "dynamic_update": dyn,
                 "cpu_baseline": cpu, "paper_context": PAPER_CONTEXT, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "wall_s_timed_loop": wall,
                 "library": rhg.version()}
@@ -583,6 +586,61 @@ def near_tie_stats(rhg, torch, c, seed, dev, opts):
     return out
 
 
+def dynamic_update(rhg, torch, c, seed, dev, fracs=(0.01, 0.05, 0.12), reps=3):
+    """SURVEY §8(f) f1 / PAPER.md:387-389: updating the config-3 graph after a
+    fraction of the vertices moved (one step of the dynamic model, rotation + Alg. 2
+    with the Appendix B step ranges) against generating the graph of the new
+    positions from scratch (rhg_generate_from_points).  Device times (CUDA events),
+    median of `reps`, outside the headline's timed loop."""
+    n = c["n"]
+    a = (c["gamma"] - 1.0) / 2.0
+    R = rhg.target_radius(n, c["kbar"], c["gamma"])
+    th, r = rhg.sample_points(n, a, R, seed, device=dev)
+    g0 = rhg.generate_from_points(th, r, R, "csr")
+    tp, tr = rhg.movement_init(n, seed + 100, device=dev)
+    th1, r1 = th.clone(), r.clone()
+    rhg.move_points(th1, r1, tp, tr, R, a)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    perm = torch.randperm(n, device=dev, generator=gen)
+    stream = torch.cuda.current_stream()
+    ws_u, ws_g = rhg.Workspace(dev), rhg.Workspace(dev)
+    out = {"workload": "config 3 graph (CSR), a random subset of the vertices moved by one "
+                       "step of the dynamic model", "rows": {}}
+
+    def timed(fn):
+        ms = []
+        res = None
+        for _ in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.median(ms[1:]), res
+
+    for f in fracs:
+        ids = torch.sort(perm[: int(f * n)]).values
+        th_n, r_n = th.clone(), r.clone()
+        th_n[ids], r_n[ids] = th1[ids], r1[ids]
+        idx32 = ids.to(torch.int32)
+        tho, ro = th[ids].contiguous(), r[ids].contiguous()
+        t_u, d = timed(lambda: rhg.update_moved(th_n, r_n, R, idx32, tho, ro, g0.row_ptr, g0.col,
+                                                workspace=ws_u))
+        t_g, g1 = timed(lambda: rhg.generate_from_points(th_n, r_n, R, "csr", workspace=ws_g,
+                                                          kbar_hint=c["kbar"]))
+        out["rows"][f"{f:.0%}"] = {"moved": int(ids.numel()), "update_ms": t_u,
+                                   "full_generation_ms": t_g, "speedup": t_g / t_u,
+                                   "removed": int(d.removed.shape[0]), "added": int(d.added.shape[0]),
+                                   "edges_after": g1.num_edges // 2}
+        del g1, d, th_n, r_n
+        torch.cuda.empty_cache()
+    del g0
+    torch.cuda.empty_cache()
+    return out
+
+
 def measure_e2e_points(rhg, torch, c, seed, dev, ws, cap, args, opts):
     """The C-ABI call that carries input payload: rhg_generate_from_points with the
     n points (theta, r: 16 B each) in page-locked HOST memory and the CSR written to
@@ -673,6 +731,7 @@ def main():
                     help="rhg_options.vertex_order of the timed steps (the other is reported too)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dynamic", action="store_true", help="skip the f1 update report")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -238,11 +238,12 @@ rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint64_t *row_pt
    directory), the range queries of Alg. 1 run for the moved vertices only, and each
    moved vertex's old and new rows are compared with the certified test of Eq. 3.
    Errors: RHG_ERR_INVALID (arguments), RHG_ERR_DOMAIN (a new point outside the disk),
-   RHG_ERR_WORKSPACE (workspace smaller than rhg_update_workspace_bytes(n, row_capacity)
+   RHG_ERR_WORKSPACE (workspace smaller than rhg_update_workspace_bytes(n, row_capacity,
+   old_row_ptr[n])
    or the moved vertices' new rows need more than row_capacity entries; the required
    number is written to *rows_needed when given), RHG_ERR_CAPACITY (added or removed
    exceeds capacity; both counts are written, nothing else), RHG_ERR_CUDA.
-   Synchronises `stream` twice (row total, delta totals). */
+   Synchronises `stream` three times (old graph size, row total, delta totals). */
 typedef struct {
   uint32_t *added;         /* device, 2*capacity entries: (u, v) pairs, u < v                */
   uint32_t *removed;       /* device, 2*capacity entries                                    */
@@ -251,14 +252,16 @@ typedef struct {
   uint64_t *num_removed;   /* HOST, required                                                */
   uint64_t row_capacity;   /* directed entries the moved vertices' new rows may take        */
   uint64_t *rows_needed;   /* HOST, optional: the entries the new rows took / need          */
-  void *workspace;         /* device scratch, >= rhg_update_workspace_bytes(n, row_capacity) */
+  void *workspace;         /* device scratch, >= rhg_update_workspace_bytes(...)            */
   size_t workspace_bytes;
   const rhg_options *options; /* slab layout knobs (num_bands, band_ratio); NULL: defaults  */
   rhg_timing *timing;      /* HOST, optional: ms_sort, ms_index, ms_count, ms_emit (rows +
                               delta), ms_total, candidates, certain                        */
 } rhg_update;
 
-size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity, const rhg_options *options);
+/* old_entries = old_row_ptr[n] (directed entries of the old graph) */
+size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity, uint64_t old_entries,
+                                  const rhg_options *options);
 rhg_status rhg_update_moved(uint64_t n, const double *theta, const double *r, double R,
                             const uint32_t *moved, uint64_t m, const double *theta_old,
                             const double *r_old, const uint64_t *old_row_ptr,

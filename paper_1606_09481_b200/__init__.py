@@ -127,7 +127,7 @@ def lib() -> ctypes.CDLL:
         L.rhg_philox_words.restype = st
         L.rhg_philox_words.argtypes = [u64, u64, u64, vp, vp]
         L.rhg_update_workspace_bytes.restype = ctypes.c_size_t
-        L.rhg_update_workspace_bytes.argtypes = [u64, u64, ctypes.POINTER(Options)]
+        L.rhg_update_workspace_bytes.argtypes = [u64, u64, u64, ctypes.POINTER(Options)]
         L.rhg_update_moved.restype = st
         L.rhg_update_moved.argtypes = [u64, vp, vp, f64, vp, u64, vp, vp, vp, vp,
                                        ctypes.POINTER(Update), vp]
@@ -461,11 +461,12 @@ def update_moved(theta, r, R: float, moved, theta_old, r_old, old_row_ptr, old_c
     opts = _options(options)
     old_deg = torch.diff(old_row_ptr)[moved.long()] if m else torch.zeros(1, device=dev)
     rcap = int(row_capacity) if row_capacity is not None else int(2 * old_deg.sum().item()) + 64 * m + 4096
+    old_entries = int(old_row_ptr[-1].item())
     cap = int(capacity) if capacity is not None else rcap // 2 + 4096
     ws = workspace if workspace is not None else Workspace(dev)
     tm = Timing()
     for _ in range(3):
-        wb = ws.get(int(L.rhg_update_workspace_bytes(n, rcap, ctypes.byref(opts))))
+        wb = ws.get(int(L.rhg_update_workspace_bytes(n, rcap, old_entries, ctypes.byref(opts))))
         added = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
         removed = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=dev)
         na, nr, rn = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()

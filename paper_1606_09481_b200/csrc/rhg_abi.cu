@@ -642,28 +642,41 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
 // staging) plus the update's arrays.
 struct UpdLayout {
   Layout base;
-  size_t midx, flag, fpos, qorder, nlm, new_col, n_rem, n_add, off_rem, off_add, total;
+  size_t pm, mbits, flag, fpos, qorder, morder, nlm, new_col, units, uoff, unit_j, n_rem, n_add,
+      off_rem, off_add, total;
+  uint64_t unit_cap;
 };
 
-UpdLayout plan_update(uint64_t n, uint64_t row_capacity, int nbands) {
+// delta work units: one per moved vertex, plus 512-entry chunks of long rows
+uint64_t update_unit_cap(uint64_t n, uint64_t row_capacity, uint64_t old_entries) {
+  return 2 * n + (row_capacity + old_entries) / 512 + 2;
+}
+
+UpdLayout plan_update(uint64_t n, uint64_t row_capacity, uint64_t old_entries, int nbands) {
   UpdLayout U{};
   U.base = plan_layout(n, RHG_CSR, 0, 0, nbands);
+  U.unit_cap = update_unit_cap(n, row_capacity, old_entries);
   size_t o = U.base.total;
   auto take = [&](size_t bytes) {
     size_t at = o;
     o += al(bytes);
     return at;
   };
-  U.midx = take(4 * n);
+  U.pm = take(8 * n);
+  U.mbits = take(4 * ((n + 31) / 32));
   U.flag = take(4 * n);
   U.fpos = take(8 * (n + 1));
   U.qorder = take(4 * n);
+  U.morder = take(4 * n);
   U.nlm = take(8);
   U.new_col = take(4 * (row_capacity ? row_capacity : 1));
-  U.n_rem = take(4 * n);
-  U.n_add = take(4 * n);
-  U.off_rem = take(8 * (n + 1));
-  U.off_add = take(8 * (n + 1));
+  U.units = take(4 * n);
+  U.uoff = take(8 * (n + 1));
+  U.unit_j = take(4 * U.unit_cap);
+  U.n_rem = take(4 * U.unit_cap);
+  U.n_add = take(4 * U.unit_cap);
+  U.off_rem = take(8 * (U.unit_cap + 1));
+  U.off_add = take(8 * (U.unit_cap + 1));
   U.total = o;
   return U;
 }
@@ -689,7 +702,10 @@ rhg_status run_update(uint64_t n, const double* theta, const double* r, double R
   BandConst bc;
   rhg_status s = make_band_const(n, R, &opt, &bc);
   if (s != RHG_OK) return s;
-  const UpdLayout U = plan_update(n, out->row_capacity, bc.L);
+  uint64_t old_entries = 0;
+  CK(cudaMemcpyAsync(&old_entries, old_rp + n, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const UpdLayout U = plan_update(n, out->row_capacity, old_entries, bc.L);
   const Layout& Lw = U.base;
   if (!out->workspace || out->workspace_bytes < U.total) return RHG_ERR_WORKSPACE;
   DevScalars* pin = pinned_scalars();
@@ -724,12 +740,12 @@ rhg_status run_update(uint64_t n, const double* theta, const double* r, double R
   CK(launch_query_order(keys_a, lay, bc.L, (uint32_t*)(ws + Lw.q_cell_lo),
                         (uint32_t*)(ws + Lw.q_cell_cnt), (uint64_t*)(ws + Lw.q_cell_off),
                         (uint32_t*)(ws + Lw.q_order), ws + Lw.scan_tmp, st, &launches));
-  // the moved vertices' sorted positions in processing order (hubs included: the
-  // light kernel handles any vertex)
+  // the moved vertices in processing order: light ones for the light kernels, hubs
+  // through hub_mask for the chunked path
   CK(launch_update_select((uint32_t)n, m, moved, lay, (const uint32_t*)(ws + Lw.q_order), vals_a,
-                          (uint32_t*)(ws + U.midx), (uint32_t*)(ws + U.flag), fpos,
-                          (uint32_t*)(ws + U.qorder), (unsigned long long*)(ws + U.nlm),
-                          ws + Lw.scan_tmp, st, &launches));
+                          (uint2*)(ws + U.pm), (uint32_t*)(ws + U.mbits), (uint32_t*)(ws + U.flag),
+                          fpos, (uint32_t*)(ws + U.qorder), (uint32_t*)(ws + U.morder),
+                          (unsigned long long*)(ws + U.nlm), ws + Lw.scan_tmp, st, &launches));
   tm.mark();  // 2
   QueryArgs qa{};
   qa.n = (uint32_t)n;
@@ -797,21 +813,31 @@ rhg_status run_update(uint64_t n, const double* theta, const double* r, double R
   uint32_t* n_add = (uint32_t*)(ws + U.n_add);
   uint64_t* off_rem = (uint64_t*)(ws + U.off_rem);
   uint64_t* off_add = (uint64_t*)(ws + U.off_add);
-  const uint32_t* midx = (const uint32_t*)(ws + U.midx);
-  CK(launch_delta(false, m, moved, midx, theta, r, theta_old, r_old, old_rp, old_col, offs, new_col,
-                  bc.T4, n_rem, n_add, nullptr, nullptr, nullptr, nullptr, st));
-  CK(exclusive_scan_u32_u64((uint32_t)(m ? m : 1), n_rem, off_rem, ws + Lw.scan_tmp, &sc->candidates,
-                            st, &launches));
-  CK(exclusive_scan_u32_u64((uint32_t)(m ? m : 1), n_add, off_add, ws + Lw.scan_tmp, &sc->certain,
-                            st, &launches));
+  const uint2* pm = (const uint2*)(ws + U.pm);
+  const uint32_t* morder = (const uint32_t*)(ws + U.morder);
+  const uint32_t* mbits = (const uint32_t*)(ws + U.mbits);
+  uint64_t* uoff = (uint64_t*)(ws + U.uoff);
+  uint32_t* unit_j = (uint32_t*)(ws + U.unit_j);
+  if (m == 0) CK(cudaMemsetAsync(uoff, 0, 8, st));  // no units
+  CK(launch_delta_plan(m, morder, old_rp, offs, (uint32_t*)(ws + U.units), uoff, unit_j,
+                       ws + Lw.scan_tmp, st, &launches));
+  CK(launch_delta(false, m, U.unit_cap, uoff, unit_j, morder, pm, mbits, pts, keys_a, lay, bc.L,
+                  theta_old, r_old, old_rp, old_col, offs, new_col, bc.T4, n_rem, n_add, nullptr,
+                  nullptr, nullptr, nullptr, st));
+  // unit counts -> offsets (uoff[m] units, counted on the device)
+  CK(exclusive_scan_u32_u64_dev(U.unit_cap, (const unsigned long long*)(uoff + m), n_rem, off_rem,
+                                ws + Lw.scan_tmp, &sc->candidates, st, &launches));
+  CK(exclusive_scan_u32_u64_dev(U.unit_cap, (const unsigned long long*)(uoff + m), n_add, off_add,
+                                ws + Lw.scan_tmp, &sc->certain, st, &launches));
   CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const uint64_t nrem = m ? pin->candidates : 0, nadd = m ? pin->certain : 0;
   *out->num_removed = nrem;
   *out->num_added = nadd;
   if (nrem > out->capacity || nadd > out->capacity) return RHG_ERR_CAPACITY;
-  CK(launch_delta(true, m, moved, midx, theta, r, theta_old, r_old, old_rp, old_col, offs, new_col,
-                  bc.T4, n_rem, n_add, off_rem, off_add, out->removed, out->added, st));
+  CK(launch_delta(true, m, U.unit_cap, uoff, unit_j, morder, pm, mbits, pts, keys_a, lay, bc.L,
+                  theta_old, r_old, old_rp, old_col, offs, new_col, bc.T4, n_rem, n_add, off_rem,
+                  off_add, out->removed, out->added, st));
   tm.mark();  // 4
   if (out->timing) {
     CK(cudaStreamSynchronize(st));
@@ -934,9 +960,9 @@ RHG_EXPORT rhg_status rhg_graph_stats(uint64_t n, rhg_format format, const uint6
   return RHG_OK;
 }
 
-RHG_EXPORT size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity,
+RHG_EXPORT size_t rhg_update_workspace_bytes(uint64_t n, uint64_t row_capacity, uint64_t old_entries,
                                              const rhg_options* options) {
-  return plan_update(n, row_capacity, bands_for(n, options)).total;
+  return plan_update(n, row_capacity, old_entries, bands_for(n, options)).total;
 }
 
 RHG_EXPORT rhg_status rhg_update_moved(uint64_t n, const double* theta, const double* r, double R,

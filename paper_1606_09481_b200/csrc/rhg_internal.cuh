@@ -253,19 +253,26 @@ cudaError_t launch_shard_plan(uint32_t n, const QueryArgs& qa, const BandConst& 
                               int* launches);
 
 // Incremental update of the dynamic model (k_update.cu)
-// flag[t] = 1 if query item t (hub position t < heavy_end, else light order entry)
-// moved; qorder = the moved light entries in processing order, *nlight_moved their count
+// pm[id] = (sorted position, index in moved or ~0); flag[t] = 1 if query item t (hub
+// position t < heavy_end, else light order entry) moved; morder = the moved vertices
+// in processing order; qorder = the moved light entries, *nlight_moved their count
 cudaError_t launch_update_select(uint32_t n, uint64_t m, const uint32_t* moved, const BandLayout* lay,
-                                 const uint32_t* order, const uint32_t* sid, uint32_t* midx,
-                                 uint32_t* flag, uint64_t* fpos, uint32_t* qorder,
-                                 unsigned long long* nlight_moved, void* scan_tmp, cudaStream_t st,
-                                 int* launches);
-cudaError_t launch_delta(bool write, uint64_t m, const uint32_t* moved, const uint32_t* midx,
-                         const double* theta, const double* r, const double* theta_old,
-                         const double* r_old, const uint64_t* old_rp, const uint32_t* old_col,
-                         const uint64_t* new_rp, const uint32_t* new_col, double T4, uint32_t* n_rem,
-                         uint32_t* n_add, const uint64_t* off_rem, const uint64_t* off_add,
-                         uint32_t* removed, uint32_t* added, cudaStream_t st);
+                                 const uint32_t* order, const uint32_t* sid, uint2* pm,
+                                 uint32_t* mbits, uint32_t* flag, uint64_t* fpos, uint32_t* qorder,
+                                 uint32_t* morder, unsigned long long* nlight_moved, void* scan_tmp,
+                                 cudaStream_t st, int* launches);
+// delta work units (k_update.cu): units[j], uoff (m + 1), unit_j (uoff[m] entries)
+cudaError_t launch_delta_plan(uint64_t m, const uint32_t* morder, const uint64_t* old_rp,
+                              const uint64_t* new_rp, uint32_t* units, uint64_t* uoff,
+                              uint32_t* unit_j, void* scan_tmp, cudaStream_t st, int* launches);
+cudaError_t launch_delta(bool write, uint64_t m, uint64_t unit_cap, const uint64_t* uoff,
+                         const uint32_t* unit_j, const uint32_t* morder, const uint2* pm,
+                         const uint32_t* mbits, const PointRec* pts, const uint32_t* skey,
+                         const BandLayout* lay, int L, const double* theta_old, const double* r_old,
+                         const uint64_t* old_rp, const uint32_t* old_col, const uint64_t* new_rp,
+                         const uint32_t* new_col, double T4, uint32_t* n_rem, uint32_t* n_add,
+                         const uint64_t* off_rem, const uint64_t* off_add, uint32_t* removed,
+                         uint32_t* added, cudaStream_t st);
 
 // Validation statistics (k_stats.cu)
 size_t stats_workspace_bytes(uint64_t n);

@@ -745,3 +745,27 @@ def test_update_moved_matches_oracle(rhg, orc, frac):
         u, v = (k >> np.uint64(32)).astype(np.int64), (k & np.uint64(0xFFFFFFFF)).astype(np.int64)
         assert np.all(mv[u] | mv[v])
     print(f"moved {len(ids)} ({frac:.0%}): removed {len(rem)} added {len(add)} excused {excused}")
+
+
+def test_update_moved_edge_cases(rhg, orc):
+    """f1 edge cases: nothing moved (empty delta); one vertex moved; every vertex moved
+    (the delta turns the old graph into the new one)."""
+    n, kbar, gamma, seed = 20_000, 10, 2.6, 43
+    th, r, R, a = oracle_points(orc, n, kbar, gamma, seed)
+    g0 = rhg.generate_from_points(torch.from_numpy(th).cuda(), torch.from_numpy(r).cuda(), R, "csr")
+    old = csr_checked_pairs(g0)
+    tp, tr = orc.movement_init(n, 7)
+    th1, r1, _ = orc.move_points(th, r, tp, tr, R, a)
+    for ids in (np.zeros(0, dtype=np.int64), np.array([int(np.argmin(r))]), np.arange(n)):
+        th_new, r_new = th.copy(), r.copy()
+        th_new[ids], r_new[ids] = th1[ids], r1[ids]
+        d = rhg.update_moved(torch.from_numpy(th_new).cuda(), torch.from_numpy(r_new).cuda(), R,
+                             torch.from_numpy(ids.astype(np.int32)).cuda(),
+                             torch.from_numpy(th[ids]).cuda(), torch.from_numpy(r[ids]).cuda(),
+                             g0.row_ptr, g0.col)
+        rem = pairs_checked(rhg.Graph(n=n, format="pairs", R=R, num_edges=len(d.removed), pairs=d.removed))
+        add = pairs_checked(rhg.Graph(n=n, format="pairs", R=R, num_edges=len(d.added), pairs=d.added))
+        new = np.union1d(np.setdiff1d(old, rem, assume_unique=True), add)
+        compare_sets(new, orc.brute_force(th_new, r_new, R))
+        if len(ids) == 0:
+            assert len(rem) == 0 and len(add) == 0
