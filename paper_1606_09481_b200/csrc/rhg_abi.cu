@@ -642,8 +642,9 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
 // staging) plus the update's arrays.
 struct UpdLayout {
   Layout base;
-  size_t pm, mbits, flag, fpos, qorder, morder, nlm, new_col, units, uoff, unit_j, n_rem, n_add,
-      off_rem, off_add, total;
+  size_t pm, mbits, flag, fpos, qorder, morder, nlm, new_col, units, uoff, unit_j, mlist, mcount,
+      n_rem, n_add, off_rem, off_add, rbits, abits, total;
+  uint64_t rbits_words, abits_words;
   uint64_t unit_cap;
 };
 
@@ -673,10 +674,16 @@ UpdLayout plan_update(uint64_t n, uint64_t row_capacity, uint64_t old_entries, i
   U.units = take(4 * n);
   U.uoff = take(8 * (n + 1));
   U.unit_j = take(4 * U.unit_cap);
+  U.mlist = take(4 * n);
+  U.mcount = take(8);
   U.n_rem = take(4 * U.unit_cap);
   U.n_add = take(4 * U.unit_cap);
   U.off_rem = take(8 * (U.unit_cap + 1));
   U.off_add = take(8 * (U.unit_cap + 1));
+  U.rbits_words = old_entries / 32 + 2;
+  U.abits_words = row_capacity / 32 + 2;
+  U.rbits = take(4 * U.rbits_words);
+  U.abits = take(4 * U.abits_words);
   U.total = o;
   return U;
 }
@@ -819,11 +826,17 @@ rhg_status run_update(uint64_t n, const double* theta, const double* r, double R
   uint64_t* uoff = (uint64_t*)(ws + U.uoff);
   uint32_t* unit_j = (uint32_t*)(ws + U.unit_j);
   if (m == 0) CK(cudaMemsetAsync(uoff, 0, 8, st));  // no units
-  CK(launch_delta_plan(m, morder, old_rp, offs, (uint32_t*)(ws + U.units), uoff, unit_j,
-                       ws + Lw.scan_tmp, st, &launches));
-  CK(launch_delta(false, m, U.unit_cap, uoff, unit_j, morder, pm, mbits, pts, keys_a, lay, bc.L,
-                  theta_old, r_old, old_rp, old_col, offs, new_col, bc.T4, n_rem, n_add, nullptr,
-                  nullptr, nullptr, nullptr, st));
+  uint32_t* mlist = (uint32_t*)(ws + U.mlist);
+  unsigned int* mcount = (unsigned int*)(ws + U.mcount);
+  CK(launch_delta_plan(m, morder, old_rp, offs, (uint32_t*)(ws + U.units), uoff, unit_j, mlist,
+                       mcount, ws + Lw.scan_tmp, st, &launches));
+  uint32_t* rbits = (uint32_t*)(ws + U.rbits);
+  uint32_t* abits = (uint32_t*)(ws + U.abits);
+  CK(cudaMemsetAsync(rbits, 0, 4 * U.rbits_words, st));
+  CK(cudaMemsetAsync(abits, 0, 4 * U.abits_words, st));
+  CK(launch_delta_decide(m, U.unit_cap, uoff, unit_j, mlist, mcount, morder, pm, mbits, pts, keys_a,
+                         lay, bc.L, theta_old, r_old, old_rp, old_col, offs, new_col, bc.T4, n_rem,
+                         n_add, rbits, abits, st));
   // unit counts -> offsets (uoff[m] units, counted on the device)
   CK(exclusive_scan_u32_u64_dev(U.unit_cap, (const unsigned long long*)(uoff + m), n_rem, off_rem,
                                 ws + Lw.scan_tmp, &sc->candidates, st, &launches));
@@ -835,9 +848,8 @@ rhg_status run_update(uint64_t n, const double* theta, const double* r, double R
   *out->num_removed = nrem;
   *out->num_added = nadd;
   if (nrem > out->capacity || nadd > out->capacity) return RHG_ERR_CAPACITY;
-  CK(launch_delta(true, m, U.unit_cap, uoff, unit_j, morder, pm, mbits, pts, keys_a, lay, bc.L,
-                  theta_old, r_old, old_rp, old_col, offs, new_col, bc.T4, n_rem, n_add, off_rem,
-                  off_add, out->removed, out->added, st));
+  CK(launch_delta_write(m, U.unit_cap, uoff, unit_j, morder, old_rp, old_col, offs, new_col, rbits,
+                        abits, off_rem, off_add, out->removed, out->added, st));
   tm.mark();  // 4
   if (out->timing) {
     CK(cudaStreamSynchronize(st));

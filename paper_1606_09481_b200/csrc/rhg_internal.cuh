@@ -264,15 +264,26 @@ cudaError_t launch_update_select(uint32_t n, uint64_t m, const uint32_t* moved, 
 // delta work units (k_update.cu): units[j], uoff (m + 1), unit_j (uoff[m] entries)
 cudaError_t launch_delta_plan(uint64_t m, const uint32_t* morder, const uint64_t* old_rp,
                               const uint64_t* new_rp, uint32_t* units, uint64_t* uoff,
-                              uint32_t* unit_j, void* scan_tmp, cudaStream_t st, int* launches);
-cudaError_t launch_delta(bool write, uint64_t m, uint64_t unit_cap, const uint64_t* uoff,
-                         const uint32_t* unit_j, const uint32_t* morder, const uint2* pm,
-                         const uint32_t* mbits, const PointRec* pts, const uint32_t* skey,
-                         const BandLayout* lay, int L, const double* theta_old, const double* r_old,
-                         const uint64_t* old_rp, const uint32_t* old_col, const uint64_t* new_rp,
-                         const uint32_t* new_col, double T4, uint32_t* n_rem, uint32_t* n_add,
-                         const uint64_t* off_rem, const uint64_t* off_add, uint32_t* removed,
-                         uint32_t* added, cudaStream_t st);
+                              uint32_t* unit_j, uint32_t* mlist, unsigned int* mcount,
+                              void* scan_tmp, cudaStream_t st, int* launches);
+// decide: per-unit counts + decision bits over old_col (rbits) / new_col (abits),
+// both zeroed by the caller; write: replay at the scanned per-unit offsets
+cudaError_t launch_delta_decide(uint64_t m, uint64_t unit_cap, const uint64_t* uoff,
+                                const uint32_t* unit_j, const uint32_t* mlist,
+                                const unsigned int* mcount, const uint32_t* morder, const uint2* pm,
+                                const uint32_t* mbits, const PointRec* pts, const uint32_t* skey,
+                                const BandLayout* lay, int L, const double* theta_old,
+                                const double* r_old, const uint64_t* old_rp, const uint32_t* old_col,
+                                const uint64_t* new_rp, const uint32_t* new_col, double T4,
+                                uint32_t* n_rem, uint32_t* n_add, uint32_t* rbits, uint32_t* abits,
+                                cudaStream_t st);
+cudaError_t launch_delta_write(uint64_t m, uint64_t unit_cap, const uint64_t* uoff,
+                               const uint32_t* unit_j, const uint32_t* morder,
+                               const uint64_t* old_rp, const uint32_t* old_col,
+                               const uint64_t* new_rp, const uint32_t* new_col,
+                               const uint32_t* rbits, const uint32_t* abits,
+                               const uint64_t* off_rem, const uint64_t* off_add, uint32_t* removed,
+                               uint32_t* added, cudaStream_t st);
 
 // Validation statistics (k_stats.cu)
 size_t stats_workspace_bytes(uint64_t n);
