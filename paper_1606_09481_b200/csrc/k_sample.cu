@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(256)
 // candidate count of a vertex in band j (its radius is >= c_j and windows shrink
 // with radius); bands with E_j above the
 // threshold form the hub prefix [0, heavy_end) of the sorted order.
+#ifndef RHG_DIR_PER_PT
+#define RHG_DIR_PER_PT 4u  // directory buckets per point (at least; power of two per slab)
+#endif
 __global__ void k_band_layout(const __grid_constant__ BandConst bc,
                               const uint32_t* __restrict__ band_hist, BandLayout* lay,
                               HeavyMeta* meta) {
@@ -101,7 +104,7 @@ __global__ void k_band_layout(const __grid_constant__ BandConst bc,
   if (j < L) {
     // >= 4 buckets per point: range ends are whole buckets (no key probing in the
     // queries), so fine buckets keep the boundary-bucket overhead small
-    uint32_t want = cnt > (1u << 25) ? (1u << 27) : 4u * cnt;
+    uint32_t want = cnt > (1u << 25) ? (1u << 27) : RHG_DIR_PER_PT * cnt;
     while (nb < want && sh > 0) {
       nb <<= 1;
       --sh;
