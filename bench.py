@@ -53,7 +53,7 @@ def peaks():
 # DMUL 18.5e12/s, DFMA 17.0e12/s (~59-64 per clk per SM).  Used for the count pass,
 # which is FP64-bound.
 FP64_PEAK_OPS = 17.0e12
-PROFILE_JSON = "r01_ncu_query_cfg3.json"  # committed ncu capture of the query kernels
+PROFILE_JSON = "r02_ncu_query_cfg3.json"  # committed ncu capture of the query kernels
 FP64_OPS_PER_TEST = 13  # certified predicate: DADD, 2 DMUL + 3 DFMA (sin poly), 5 DMUL, DADD, DFMA
 
 
@@ -414,7 +414,12 @@ def run_ours(args):
             k = prof["kernels"][lab]
             rate = k["inst_executed"] / (k["duration_ms"] * 1e-3)
             issue[lab] = {"warp_inst": k["inst_executed"], "ms": k["duration_ms"],
-                          "achieved": rate, "frac": rate / peak}
+                          "achieved": rate, "frac": rate / peak,
+                          "fp64_pipe_pct": k.get("fp64_pipe_pct"),
+                          "active_threads_per_inst": k.get("threads_per_inst"),
+                          "branch_targets_uniform_pct": k.get("branch_targets_uniform_pct"),
+                          "l2_hit_pct": k.get("l2_hit_pct"),
+                          "top_stalls_per_issue": k.get("top_stalls_per_issue")}
     except Exception:
         pass
     # north-star convention: points read (32 B) + 8 B per emitted directed edge, over query+emit

@@ -19,8 +19,8 @@ def label(name):
     return f"{k}<{mode}{fmt}{wide}{seq}>"
 
 
-out = {"source": "ncu --set full --clock-control none, config 3, one launch each "
-                 "(scripts/gpu_round.sh)", "kernels": {}}
+out = {"source": "ncu --set full --clock-control none, one launch each (scripts/ncu_kq.sh; "
+                 "config in the file name)", "kernels": {}}
 for path in sys.argv[2:]:
     rows = list(csv.reader(open(path)))
     h, u = rows[0], rows[1]
@@ -35,7 +35,17 @@ for path in sys.argv[2:]:
             "dram_write_GB": g("dram__bytes_write.sum") * SCALE[u[col["dram__bytes_write.sum"]]],
             "inst_executed": g("smsp__inst_executed.sum"),
             "ipc": g("sm__inst_executed.avg.per_cycle_active"),
-            "achieved_occupancy_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active")})
+            "achieved_occupancy_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "threads_per_inst": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
+            "branch_targets_uniform_pct": g("smsp__sass_average_branch_targets_threads_uniform.pct"),
+            "l2_hit_pct": g("lts__t_sector_hit_rate.pct"),
+            "top_stalls_per_issue": dict(sorted(
+                ((k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
+                  round(float(r[i]), 2)) for k, i in col.items()
+                 if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")
+                 and r[i] not in ("", "n/a")), key=lambda kv: -kv[1])[:5])})
 json.dump(out, open(sys.argv[1], "w"), indent=1)
 print(json.dumps({k: (v["duration_ms"], round(v["dram_read_GB"] + v["dram_write_GB"], 3))
                   for k, v in out["kernels"].items()}))
