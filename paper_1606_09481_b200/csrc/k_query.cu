@@ -615,8 +615,10 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   SecWriter<FMT> sw;
   unsigned long long hcur = 0;
   if (MODE != QM_COUNT) {
-    const unsigned long long pos0 = valid ? A.offs[qid] : 0ull;
-    if (SEQ) hcur = valid ? pos0 + A.cdeg[qid] : 0ull;
+    // list output: degrees and offsets by processing position (coalesced), else by id
+    const uint32_t slot = A.poff ? A.lay->heavy_end + idx : qid;
+    const unsigned long long pos0 = valid ? A.offs[slot] : 0ull;
+    if (SEQ) hcur = valid ? pos0 + A.cdeg[slot] : 0ull;
     if (SEQ) {
       sw.init(pos0, qid);
     } else {
@@ -784,7 +786,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   }
   if (MODE == QM_COUNT) {
     if (valid) {
-      const uint32_t id = A.labels ? k : __ldg(A.sid + k);
+      const uint32_t id = A.poff ? A.lay->heavy_end + idx : (A.labels ? k : __ldg(A.sid + k));
       A.deg[id] = deg;
       if (A.labels) A.cdeg[id] = (uint32_t)certain;
     }
@@ -889,7 +891,7 @@ __global__ void __launch_bounds__(HV_THREADS)
       H.np[i] = ci;
       H.vtot[i] = ca;
     }
-    if (lane == 0) A.deg[A.labels ? i : A.sid[i]] = 0u;
+    if (lane == 0) A.deg[(A.labels || A.poff) ? i : A.sid[i]] = 0u;
   }
 }
 
@@ -970,7 +972,7 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
     const uint32_t np = H.np[i];
     const uint32_t qid = A.labels ? i : A.sid[i];
     unsigned long long base = 0;
-    if (MODE != QM_COUNT) base = A.offs[qid] + (H.chunk_pos[c] - H.chunk_pos[c0]);
+    if (MODE != QM_COUNT) base = A.offs[A.poff ? i : qid] + (H.chunk_pos[c] - H.chunk_pos[c0]);
     const uint32_t qband = A.skey[i] >> kBandShift;
     const PointRec q = A.pts[i + A.lay->start[qband]];
     const double q4s = 4.0 * q.s;
@@ -1042,7 +1044,7 @@ __global__ void __launch_bounds__(HV_THREADS, RHG_HV_MINB)
     }
     if (MODE == QM_COUNT && lane == 0) {
       H.chunk_hits[c] = run;
-      if (run) atomicAdd(&A.deg[qid], run);
+      if (run) atomicAdd(&A.deg[A.poff ? i : qid], run);
     }
   }
   if (MODE == QM_COUNT && lane == 0) {

@@ -453,6 +453,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   qa = QueryArgs{};
   qa.n = (uint32_t)n;
   qa.labels = (uint32_t)order;
+  qa.poff = f == RHG_EDGES_UNDIRECTED ? 1u : 0u;  // rows of the list need no id order
   qa.force_wide = (out->options && out->options->wide_positions == 1) ? 1u : 0u;
   qa.stats = out->timing ? 1u : 0u;
   qa.pts = pts;

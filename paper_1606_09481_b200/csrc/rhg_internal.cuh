@@ -141,6 +141,8 @@ struct QueryArgs {
   uint32_t* warp_over;                // per light warp: 1 if its bits did not fit (emit re-tests)
   DevScalars* sc;
   uint32_t labels;                    // 0: ids = sample / input indices; 1: sorted positions
+  uint32_t poff;                      // 1 (list output): deg / cdeg / offs indexed by processing
+                                      // position (hub i, then heavy_end + light order index)
   uint32_t force_wide;                // 64-bit slab positions in the light kernels
   uint32_t stats;                     // accumulate candidate / certain totals (timing)
   const unsigned long long* total_dev;  // emit: skip everything if *total_dev > cap
