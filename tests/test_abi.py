@@ -94,3 +94,26 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "rhg_oracle" not in txt and "liborc" not in txt, f
+
+
+def test_update_workspace_and_argument_checks(rhg):
+    """f1 (rhg_update_moved): the workspace grows with the row capacity and the old
+    graph's size; invalid arguments are rejected on the host before any CUDA call."""
+    L = rhg.lib()
+    w0 = L.rhg_update_workspace_bytes(100_000, 10_000, 1_000_000, None)
+    w1 = L.rhg_update_workspace_bytes(100_000, 1_000_000, 1_000_000, None)
+    w2 = L.rhg_update_workspace_bytes(100_000, 1_000_000, 100_000_000, None)
+    assert 0 < w0 < w1 < w2
+    assert w1 - w0 >= 4 * (1_000_000 - 10_000)          # the new rows
+    u = rhg.Update()
+    na, nr = ctypes.c_uint64(), ctypes.c_uint64()
+    u.num_added, u.num_removed = ctypes.pointer(na), ctypes.pointer(nr)
+    # missing points / graph, n < 2, m > n
+    assert L.rhg_update_moved(1000, None, None, 10.0, None, 0, None, None, None, None,
+                              ctypes.byref(u), None) == rhg.RHG_ERR_INVALID
+    assert L.rhg_update_moved(1, 8, 8, 10.0, None, 0, None, None, 8, None, ctypes.byref(u),
+                              None) == rhg.RHG_ERR_INVALID
+    assert L.rhg_update_moved(10, 8, 8, 10.0, 8, 11, 8, 8, 8, 8, ctypes.byref(u),
+                              None) == rhg.RHG_ERR_INVALID
+    assert L.rhg_update_moved(10, 8, 8, float("nan"), None, 0, None, None, 8, None,
+                              ctypes.byref(u), None) == rhg.RHG_ERR_INVALID
