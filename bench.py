@@ -274,9 +274,11 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        # NCCL between GPUs; RHG_BENCH_BACKEND=gloo lets a test run ranks that share a GPU
+        dist.init_process_group(os.environ.get("RHG_BENCH_BACKEND", "nccl"))
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     c = CONFIG3
     shard = args.mode == "shard" and world > 1
     # replicas: an independent graph per rank (weak scaling); shard: one graph, each
@@ -334,7 +336,7 @@ def run_ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     phases = []
-    clk = ClockSampler(local)
+    clk = ClockSampler(gpu)
     clk.start()
     clk.wait_first()
     if world > 1:
@@ -359,7 +361,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
-    tot_ms, m_und_total = reduce_over_ranks(tot_ms, last.num_edges / 2.0, dev, world)
+    red_dev = dev if world == 1 or dist.get_backend() == "nccl" else "cpu"
+    tot_ms, m_und_total = reduce_over_ranks(tot_ms, last.num_edges / 2.0, red_dev, world)
     ms_per_step = tot_ms / args.steps  # m_und_total: undirected edges per step, all ranks
     value = m_und_total / (ms_per_step * 1e-3)
 
