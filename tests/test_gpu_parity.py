@@ -769,3 +769,33 @@ def test_update_moved_edge_cases(rhg, orc):
         compare_sets(new, orc.brute_force(th_new, r_new, R))
         if len(ids) == 0:
             assert len(rem) == 0 and len(add) == 0
+
+
+def test_bench_two_ranks_one_graph():
+    """bench.py's multi-GPU path end to end: two ranks under torchrun
+    shard ONE config-3 graph (work-balanced shards, one all_gather of edge counts);
+    the reported undirected edges/s is the whole graph's edges over the slowest
+    rank's time.  The ranks share this box's one GPU (gloo instead of NCCL), which
+    checks the host logic, not the scaling."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, RHG_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--no-configs", "--no-cpu", "--no-e2e", "--no-dynamic"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["parallelism"] == "shards"
+    und = line["config"]["undirected_edges_per_step_per_rank"]
+    assert abs(line["value"] * line["ms_per_step"] * 1e-3 - 500_429_556) < 1e-6 * 500_429_556 + 1
+    assert und > 0
