@@ -62,6 +62,12 @@ namespace rhg {
   } while (0)
 #endif
 
+// RHG_ABL (measurement builds only, wrong output): 1 = no certain-id copy, 2 = no hit
+// replay, 4 = no row stores.  Attributes the emit kernel's time and DRAM traffic
+// (profiles/r02_emit_ablation.txt).
+#ifndef RHG_ABL
+#define RHG_ABL 0
+#endif
 #ifndef RHG_QK_WARPS
 #define RHG_QK_WARPS 4
 #endif
@@ -400,6 +406,7 @@ struct RowWriter {
   __device__ __forceinline__ void flush(const QueryArgs& A, unsigned long long sec) {
     const uint32_t h = (uint32_t)(sec & 1);
     const unsigned long long s0 = sec * EPS;
+    if (RHG_ABL & 4) return;
     if (s0 >= start) {
       uint32_t* dst = FMT == RHG_CSR ? A.col + s0 : A.pairs + 2 * s0;
       const uint4 a = *reinterpret_cast<const uint4*>(stage + ((8u * h) ^ sw));
@@ -693,7 +700,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
       const uint32_t n0 = l0 ? (c0 + l0 - a0 + 3u) >> 2 : 0u;
       const uint32_t n1 = l1 ? (c1 + l1 - a1 + 3u) >> 2 : 0u;
       const uint32_t nit = n0 + n1;
-      const uint32_t mc = __reduce_max_sync(FULL, nit);
+      const uint32_t mc = (RHG_ABL & 1) ? 0u : __reduce_max_sync(FULL, nit);
       for (uint32_t i = 0; i < mc; ++i) {
         if (i < nit) {
           const bool second = i >= n0;
@@ -715,6 +722,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     // own-slab exclusion in doubled positions: [x1, x1 + wx) and [x1 + nj, ...)
     const uint32_t x1 = gbase + (uint32_t)e1, xw = (uint32_t)wx;
     if (MODE == QM_COUNT) tested += nt;
+    if ((RHG_ABL & 2) && MODE == QM_EMIT_BITS) continue;
     if (MODE == QM_EMIT_BITS && !retest) {
       // replay: word F + i of the warp's bit stream is the ballot of the count pass's
       // i-th test iteration of this slab (bit l: lane l's i-th candidate).  Per 32
