@@ -62,8 +62,9 @@ typedef enum {
 typedef struct {
   int num_bands;     /* L, number of slabs (1..32); 0 -> min(16, ceil(ln n)) ("log n" slabs,
                         PAPER.md:108, base unstated; Z7) */
-  double band_ratio; /* p, geometric width ratio in (0, 1); 0 -> 0.85 (the paper's 0.9,
-                        PAPER.md:116-124, costs more tests with L capped at 16; Z7) */
+  double band_ratio; /* p, geometric width ratio in (0, 1); 0 -> 0.85 for ceil(ln n) <= 17,
+                        + 0.04 per further unit, at most 0.95 (the paper's 0.9 was its own
+                        measured choice; Z7) */
   uint32_t heavy_threshold; /* hub selection: a slab's vertices whose expected candidate
                                count (upper bound over the slab, all slabs' windows) exceeds
                                this are hubs, whose candidate sequences are cut into chunks
