@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     // count, or emit with re-tests: every candidate is tested
     const bool store = F + mt <= kLightBitRows * 32u;  // warp-uniform
     if (MODE == QM_COUNT && !store) over = true;
-    auto test_loop = [&](auto short_poly) {
+    auto test_loop = [&](auto short_poly, auto own_slab) {
       // chunks of 32 iterations: lane u keeps the ballot word of iteration i0 + u and
       // the chunk's words are stored together (count pass)
       for (uint32_t i0 = 0; i0 < mt; i0 += 32u) {
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
           const bool act = i < nt;
           const uint32_t p = pa + i + (i >= thr ? hl : 0u);
           bool tst = act;
-          if (anyown) tst = tst && !((p - x1) < xw || (p - x1 - nj) < xw);
+          if (decltype(own_slab)::value) tst = tst && !((p - x1) < xw || (p - x1 - nj) < xw);
           uint32_t r[8];
           const PointRec* wp = A.pts + (tst ? p : 0u);
           asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -788,8 +788,14 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     const int32_t q32 = (int32_t)(qkey & kQMask);
     const bool small = __all_sync(
         FULL, !on || (!WIDE && w.dq < 300000 && q32 >= w.dq && q32 + w.dq < (int32_t)(1u << kQBits)));
-    if (small) test_loop(std::true_type{});
-    else test_loop(std::false_type{});
+    // the own-slab exclusion only where some lane queries its own slab
+    if (anyown) {
+      if (small) test_loop(std::true_type{}, std::true_type{});
+      else test_loop(std::false_type{}, std::true_type{});
+    } else {
+      if (small) test_loop(std::true_type{}, std::false_type{});
+      else test_loop(std::false_type{}, std::false_type{});
+    }
     F += mt;
   }
   if (MODE == QM_COUNT) {
