@@ -553,17 +553,27 @@ __device__ __forceinline__ double inv4s_of(double s) {
 #ifndef RHG_QK_MINB_SEQ
 #define RHG_QK_MINB_SEQ 7  // 72 registers: the eight sector registers of SecWriter
 #endif
+#ifndef RHG_QK_MINB_LIST
+#define RHG_QK_MINB_LIST 8  // list emit (COOP): no row stage, 64 registers
+#endif
 template <int MODE, int FMT, bool WIDE, bool SEQ>
 __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COUNT
-                                              : (SEQ ? RHG_QK_MINB_SEQ : RHG_QK_MINB_EMIT))
+                                              : (FMT == RHG_EDGES_UNDIRECTED ? RHG_QK_MINB_LIST
+                                              : (SEQ ? RHG_QK_MINB_SEQ : RHG_QK_MINB_EMIT)))
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
+  // Undirected list: the 32 rows of a warp are adjacent in the output (offsets by
+  // processing position) and the order of the pairs inside that region is free, so
+  // the warp fills it iteration by iteration -- every lane with a pair in this
+  // iteration writes it at the warp cursor + its rank among those lanes (ballot +
+  // popc): coalesced stores, no per-lane ring, no bit transpose, no per-lane loops.
+  constexpr bool COOP = MODE != QM_COUNT && FMT == RHG_EDGES_UNDIRECTED;
   // emit launched before the host has seen the edge total: nothing is written
   // unless it fits the caller's capacity (block-uniform exit)
   if (MODE != QM_COUNT && A.total_dev && *A.total_dev > A.cap) return;
   __shared__ BandSm bs;
   __shared__ SlabC scs[kMaxBands];
-  __shared__ __align__(16) uint32_t stage_all[(MODE == QM_COUNT || SEQ) ? 4 : QK_THREADS * kStageStride];
+  __shared__ __align__(16) uint32_t stage_all[(MODE == QM_COUNT || SEQ || COOP) ? 4 : QK_THREADS * kStageStride];
   load_band_sm(bs, A.lay, bc.L);
   if (threadIdx.x < (unsigned)bc.L) {
     const int j = threadIdx.x;
@@ -621,7 +631,13 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   RowWriter<FMT> rw;
   SecWriter<FMT> sw;
   unsigned long long hcur = 0;
-  if (MODE != QM_COUNT) {
+  unsigned long long wc = 0;  // COOP: the warp's output cursor (warp-uniform)
+  const uint32_t ltmask = (1u << lane) - 1u;
+  if (COOP) {
+    // lane 0 is valid in every launched warp; its row starts the warp's region
+    if (lane == 0) wc = A.offs[A.lay->heavy_end + idx];
+    wc = __shfl_sync(FULL, wc, 0);
+  } else if (MODE != QM_COUNT) {
     // list output: degrees and offsets by processing position (coalesced), else by id
     const uint32_t slot = A.poff ? A.lay->heavy_end + idx : qid;
     const unsigned long long pos0 = valid ? A.offs[slot] : 0ull;
@@ -683,6 +699,21 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     if (MODE == QM_COUNT) {
       deg += ct;
       certain += ct;
+    } else if (COOP) {
+      // ---- certain edges, list output: one pair per lane and iteration ----
+      const uint32_t c0 = gbase + (uint32_t)clo0, c1 = gbase + (uint32_t)clo1;
+      const uint32_t l0 = (uint32_t)cln0;
+      const uint32_t mc = (RHG_ABL & 1) ? 0u : __reduce_max_sync(FULL, ct);
+      for (uint32_t u = 0; u < mc; ++u) {
+        const bool act = u < ct;
+        const uint32_t am = __ballot_sync(FULL, act);
+        if (act) {
+          const uint32_t x = u < l0 ? c0 + u : c1 + (u - l0);
+          const uint32_t w = SEQ ? seq_id(x, bstart, nj) : ld_keep(A.sid2 + x, keep);
+          write_edge<FMT>(A, wc + __popc(am & ltmask), qid, w);
+        }
+        wc += __popc(am);
+      }
     } else if (SEQ) {
       // ---- certain edges: consecutive ids, two pieces, each wrapping at most once ----
       const uint32_t rel0 = (uint32_t)clo0 >= nj ? (uint32_t)clo0 - nj : (uint32_t)clo0;
@@ -723,6 +754,27 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     const uint32_t x1 = gbase + (uint32_t)e1, xw = (uint32_t)wx;
     if (MODE == QM_COUNT) tested += nt;
     if ((RHG_ABL & 2) && MODE == QM_EMIT_BITS) continue;
+    if (COOP && MODE == QM_EMIT_BITS && !retest) {
+      // replay, list output: word F + i is the ballot of the count pass's i-th test
+      // iteration of this slab; its set lanes write their pairs side by side
+      for (uint32_t i0 = 0; i0 < mt; i0 += 32u) {
+        const uint32_t wv = i0 + (uint32_t)lane < mt ? wstream[F + i0 + (uint32_t)lane] : 0u;
+        const uint32_t cnt = min(32u, mt - i0);
+        for (uint32_t u = 0; u < cnt; ++u) {
+          const uint32_t m = __shfl_sync(FULL, wv, u);
+          if (m == 0u) continue;
+          if ((m >> lane) & 1u) {
+            const uint32_t i = i0 + u;
+            const uint32_t p = pa + i + (i >= thr ? hl : 0u);
+            const uint32_t w = SEQ ? seq_id(p, bstart, nj) : ld_keep(A.sid2 + p, keep);
+            write_edge<FMT>(A, wc + __popc(m & ltmask), qid, w);
+          }
+          wc += __popc(m);
+        }
+      }
+      F += mt;
+      continue;
+    }
     if (MODE == QM_EMIT_BITS && !retest) {
       // replay: word F + i of the warp's bit stream is the ballot of the count pass's
       // i-th test iteration of this slab (bit l: lane l's i-th candidate).  Per 32
@@ -774,6 +826,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
             deg += hit;
             const uint32_t hm = __ballot_sync(FULL, hit);
             word = u == (uint32_t)lane ? hm : word;
+          } else if (COOP) {
+            const uint32_t hm = __ballot_sync(FULL, hit);
+            if (hit)
+              write_edge<FMT>(A, wc + __popc(hm & ltmask), qid,
+                              SEQ ? seq_id(p, bstart, nj) : ld_keep(A.sid2 + p, keep));
+            wc += __popc(hm);
           } else if (hit) {
             if (SEQ) write_edge<FMT>(A, hcur++, qid, seq_id(p, bstart, nj));
             else rw.put(A, qid, ld_keep(A.sid2 + p, keep));
@@ -817,7 +875,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
         atomicAdd(&A.sc->certain, cw);
       }
     }
-  } else if (valid) {
+  } else if (!COOP && valid) {
     if (SEQ) sw.finish(A);
     else rw.finish(A);
   }
