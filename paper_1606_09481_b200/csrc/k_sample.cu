@@ -4,6 +4,8 @@
 // Paper: Alg. 1 lines 6-10: draw phi ~ U[0, 2pi) and r with
 // density f(r) = alpha sinh(alpha r)/(cosh(alpha R) - 1) (Eq. 1),
 // insert into the slab b_i with c_i <= r < c_{i+1}.
+#include <cmath>
+
 #include "rhg_internal.cuh"
 
 namespace rhg {
@@ -29,25 +31,52 @@ __global__ void k_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint3
   }
 }
 
+// Band of a point from its radial variate u2 (words_to_point): r(u2) is increasing,
+// so c_j <= r < c_{j+1} iff ucut[j] <= u2 < ucut[j+1] -- decided here without the
+// asinh / sqrt, except within a relative 2^-30 of a threshold (never, in practice),
+// where r is evaluated and band_of decides (r's own rounding error is ~1e-16
+// relative, far inside that margin).  Same band as band_of(r) for every point.
+__device__ __forceinline__ uint32_t band_of_u(double u2, const PhiloxPoints& g, int L, bool& amb) {
+  int j = L - 1;
+  while (j > 0 && u2 < g.ucut[j]) --j;
+  amb = (j > 0 && u2 < g.ucut[j] * (1.0 + 0x1.0p-30)) ||
+        (j + 1 < L && u2 > g.ucut[j + 1] * (1.0 - 0x1.0p-30));
+  return (uint32_t)j;
+}
+
 __global__ void __launch_bounds__(256)
-    k_sample(uint64_t n, uint64_t seed, double two_over_alpha, double half_span,
+    k_sample(uint64_t n, const __grid_constant__ PhiloxPoints gen,
              const __grid_constant__ BandConst bc, double* __restrict__ theta,
              double* __restrict__ r, uint32_t* __restrict__ keys, uint32_t* __restrict__ idx,
              uint32_t* __restrict__ band_hist) {
   __shared__ uint32_t hist[kMaxBands];
   if (threadIdx.x < kMaxBands) hist[threadIdx.x] = 0;
   __syncthreads();
+  // keys only (the generate path): the band from u2, no radius
+  const bool cuts = !r && !theta && (bc.L == 1 || gen.ucut[1] > 0.0);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    double th, rr;
-    words_to_point(vertex_words(seed, i), two_over_alpha, half_span, bc.R, th, rr);
-    if (theta) theta[i] = th;
-    if (r) r[i] = rr;
+    double th, rr = 0.0;
+    uint32_t j = 0;
+    bool amb = true;
+    const uint4 w = vertex_words(gen.seed, i);
+    if (cuts) {
+      const uint64_t a = ((uint64_t)w.y << 32) | w.x, b = ((uint64_t)w.w << 32) | w.z;
+      th = __dmul_rn(RHG_TWO_PI_HI, __dmul_rn((double)(a >> 11), 0x1.0p-53));
+      j = band_of_u(__dmul_rn((double)(b >> 11), 0x1.0p-53), gen, bc.L, amb);
+    }
+    if (amb) {
+      words_to_point(w, gen.two_over_alpha, gen.half_span, bc.R, th, rr);
+      if (theta) theta[i] = th;
+      if (r) r[i] = rr;
+      if (keys) j = band_of(rr, bc);
+    }
     if (keys) {
-      uint32_t j = band_of(rr, bc);
       keys[i] = (j << kBandShift) | q27_of(th);
       idx[i] = (uint32_t)i;
-      atomicAdd(&hist[j], 1u);
+      // one shared-memory add per band present in the warp
+      const uint32_t peers = __match_any_sync(__activemask(), j);
+      if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[j], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
@@ -91,9 +120,6 @@ __global__ void __launch_bounds__(256)
 // candidate count of a vertex in band j (its radius is >= c_j and windows shrink
 // with radius); bands with E_j above the
 // threshold form the hub prefix [0, heavy_end) of the sorted order.
-#ifndef RHG_DIR_PER_PT
-#define RHG_DIR_PER_PT 4u  // directory buckets per point (at least; power of two per slab)
-#endif
 __global__ void k_band_layout(const __grid_constant__ BandConst bc,
                               const uint32_t* __restrict__ band_hist, BandLayout* lay,
                               HeavyMeta* meta) {
@@ -179,8 +205,7 @@ cudaError_t launch_philox_words(uint64_t seed, uint64_t i0, uint64_t count, uint
 cudaError_t launch_sample(uint64_t n, const PhiloxPoints& gen, const BandConst& bc, double* theta,
                           double* r, uint32_t* keys, uint32_t* idx, uint32_t* band_hist,
                           cudaStream_t st) {
-  k_sample<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(n, gen.seed, gen.two_over_alpha,
-                                                       gen.half_span, bc, theta, r, keys, idx,
+  k_sample<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(n, gen, bc, theta, r, keys, idx,
                                                        band_hist);
   return cudaGetLastError();
 }
@@ -191,6 +216,14 @@ cudaError_t launch_keys_from_points(uint64_t n, const double* theta, const doubl
   k_keys_from_points<<<grid_for(n, 256, num_sms() * 32), 256, 0, st>>>(n, theta, r, bc, keys, idx,
                                                                  band_hist, sc);
   return cudaGetLastError();
+}
+
+void set_band_cuts(PhiloxPoints& gen, double alpha, const BandConst& bc) {
+  for (int j = 0; j <= kMaxBands; ++j) gen.ucut[j] = 0.0;
+  for (int j = 1; j < bc.L; ++j) {
+    const double s = std::sinh(0.5 * alpha * bc.c[j]);
+    gen.ucut[j] = s * s / gen.half_span;
+  }
 }
 
 cudaError_t launch_band_layout(const BandConst& bc, const uint32_t* band_hist, BandLayout* lay,

@@ -176,7 +176,7 @@ Layout plan_layout(uint64_t n, rhg_format f, uint64_t cap, int host, int nbands)
   L.lay = take(sizeof(BandLayout));
   L.pts = take(2 * sizeof(PointRec) * n);  // doubled SoA
   L.sid2 = take(2 * 4 * n);
-  L.dir_cap = 8 * n + 4 * kMaxBands + 8;  // <= 8 n_j + 1 entries per band
+  L.dir_cap = 2 * RHG_DIR_PER_PT * n + 4 * kMaxBands + 8;  // <= 2 RHG_DIR_PER_PT n_j + 1 per band
   L.dir = take(4 * L.dir_cap);
   L.deg = take(4 * n);
   L.cdeg = take(4 * n);
@@ -397,6 +397,7 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
     gen.two_over_alpha = 2.0 / alpha;
     gen.half_span = (std::cosh(alpha * R) - 1.0) / 2.0;
     gen.R = R;
+    set_band_cuts(gen, alpha, bc);
     if (host) {
       if (!out->theta_out) theta = nullptr;
       if (!out->r_out) r = nullptr;
@@ -1005,7 +1006,11 @@ RHG_EXPORT rhg_status rhg_sample_points(uint64_t n, double alpha, double R, uint
   BandConst bc;
   rhg_status s = make_band_const(n < 2 ? 2 : n, R, nullptr, &bc);
   if (s != RHG_OK) return s;
-  PhiloxPoints gen{seed, 2.0 / alpha, (std::cosh(alpha * R) - 1.0) / 2.0, R};
+  PhiloxPoints gen{};
+  gen.seed = seed;
+  gen.two_over_alpha = 2.0 / alpha;
+  gen.half_span = (std::cosh(alpha * R) - 1.0) / 2.0;
+  gen.R = R;
   CK(launch_sample(n, gen, bc, theta, r, nullptr, nullptr, nullptr, (cudaStream_t)stream));
   return RHG_OK;
 }

@@ -12,6 +12,9 @@ namespace rhg {
 constexpr int kMaxBands = 32;          // L <= 32: n < 2^32 => ceil(log2 n) <= 32
 constexpr int kBandShift = 27;         // sort key = band << 27 | q27(theta)
 constexpr uint32_t kQBits = 27;
+#ifndef RHG_DIR_PER_PT
+#define RHG_DIR_PER_PT 4u  // directory buckets per point (at least; power of two per slab)
+#endif
 constexpr uint32_t kQMax = (1u << kQBits) - 1u;
 constexpr uint32_t kQMask = kQMax;
 constexpr uint32_t kLightBitRows = 8;   // bit words per lane of a light warp (256 tests)
@@ -186,7 +189,13 @@ __device__ __forceinline__ void words_to_point(uint4 w, double two_over_alpha, d
 struct PhiloxPoints {
   uint64_t seed;
   double two_over_alpha, half_span, R;
+  // ucut[j] = sinh^2(alpha c_j / 2) / half_span (j = 1..L-1): the u2 at which
+  // words_to_point's r reaches c_j, so the band of a point follows from u2 alone
+  // (k_sample); 0 = not set (every band from r)
+  double ucut[kMaxBands + 1];
 };
+// the slab boundaries' u2 thresholds (host)
+void set_band_cuts(PhiloxPoints& gen, double alpha, const BandConst& bc);
 
 // Streaming multiprocessors of the current device (cudaDevAttrMultiProcessorCount,
 // cached per device): grids are sized in multiples of it.

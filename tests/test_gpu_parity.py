@@ -553,6 +553,22 @@ def test_sorted_vertex_order_is_the_stable_key_sort(rhg, orc, case):
     assert np.array_equal(perm, _expected_perm(rhg, th, r, R))
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_band_from_u_equals_band_from_r(rhg, cfg):
+    """The sampler of the generate path assigns bands from the radial variate u2 and
+    the thresholds ucut_j = sinh^2(alpha c_j / 2) / half_span (no radius); with the
+    points requested it takes band_of(r).  Both must give the
+    same slabs: identical (slab, angle) order (perm) and the same graph size."""
+    n, kbar, gamma, seed = CONFIGS[cfg]
+    o = dict(vertex_order=1)
+    g1 = rhg.generate(n, kbar, gamma, seed, "pairs", options=o, return_points=True)
+    p1, m1 = g1.perm.clone(), g1.num_edges
+    del g1
+    g2 = rhg.generate(n, kbar, gamma, seed, "pairs", options=o)
+    assert g2.num_edges == m1
+    assert torch.equal(g2.perm, p1)
+
+
 def test_sorted_vertex_order_full_size_equals_default(rhg):
     """Config 3 (n = 1e7, kbar = 100): the vertex_order = 1 graph relabelled through
     perm is the default graph, edge for edge (compared on the GPU)."""
