@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
   const uint32_t ltmask = (1u << lane) - 1u;
   if (COOP) {
     // lane 0 is valid in every launched warp; its row starts the warp's region
-    if (lane == 0) wc = A.offs[A.lay->heavy_end + idx];
+    if (lane == 0) wc = A.offs[A.lay->heavy_end + gbeg + g];
     wc = __shfl_sync(FULL, wc, 0);
   } else if (MODE != QM_COUNT) {
     // list output: degrees and offsets by processing position (coalesced), else by id
@@ -857,7 +857,12 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     F += mt;
   }
   if (MODE == QM_COUNT) {
-    if (valid) {
+    if (FMT == RHG_EDGES_UNDIRECTED) {
+      // list output: the warp's rows are one region, so one degree entry per warp
+      // (after the hub rows): the scan runs over heavy_end + groups entries
+      const uint32_t wsum = __reduce_add_sync(FULL, valid ? deg : 0u);
+      if (lane == 0) A.deg[A.lay->heavy_end + gbeg + g] = wsum;
+    } else if (valid) {
       const uint32_t id = A.poff ? A.lay->heavy_end + idx : (A.labels ? k : __ldg(A.sid + k));
       A.deg[id] = deg;
       if (A.labels) A.cdeg[id] = (uint32_t)certain;

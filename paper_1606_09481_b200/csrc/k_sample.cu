@@ -187,6 +187,7 @@ __global__ void k_band_layout(const __grid_constant__ BandConst bc,
     uint32_t he = startJ < bc.heavy_cap ? startJ : bc.heavy_cap;
     lay->heavy_end = he;
     meta->nvtx = he;
+    meta->list_len = he + (total - he + 31u) / 32u;
   }
 }
 

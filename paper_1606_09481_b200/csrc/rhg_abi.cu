@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -516,7 +517,12 @@ rhg_status run(uint64_t n, bool sample, double alpha, uint64_t seed, const doubl
   CK(cudaStreamWaitEvent(st, ss.join, 0));
   tm.mark();  // 4
   offs = (f == RHG_CSR) ? row_ptr_dev : offs_ws;
-  CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
+  if (f == RHG_CSR)
+    CK(exclusive_scan_u32_u64((uint32_t)n, deg, offs, ws + Lw.scan_tmp, &sc->total, st, &launches));
+  else  // list: hub rows, then one entry per light warp (k_query)
+    CK(exclusive_scan_u32_u64_dev(std::min<uint64_t>(n, bc.heavy_cap + (n + 31) / 32 + 1),
+                                  &hmeta->list_len, deg, offs, ws + Lw.scan_tmp, &sc->total, st,
+                                  &launches));
   tm.mark();  // 5
   CK(cudaMemcpyAsync(pin, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
   return RHG_OK;

@@ -65,6 +65,7 @@ struct HeavyMeta {
   unsigned long long nchunks;  // total chunks
   unsigned long long chunk;    // chunk size (candidates, multiple of 32)
   unsigned long long hits;     // total edges of hub vertices (directed / outward)
+  unsigned long long list_len; // list output: hub rows + one entry per light warp (degree scan)
 };
 
 constexpr uint32_t kCertainPiece = 0x80000000u;  // plen flag: every candidate is an edge
