@@ -690,6 +690,14 @@ __global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COU
     if (own) {
       const I kv = (I)(k - bstart);
       if (outward) { e1 = 0; wx = kv + 1; } else { e1 = kv; wx = 1; }
+      // list: only partners sorted after v.  When the tested range lies in the first
+      // copy its excluded part is the prefix [a, kv]: start the range at kv + 1
+      // (count and emit trim alike, so the bit streams line up)
+      if (outward && w.b <= (I)nj && w.a <= kv) {
+        w.a = min(kv + 1, w.b);
+        w.h0 = max(w.h0, w.a);
+        w.h1 = max(w.h1, w.a);
+      }
     }
     // certain pieces (own slab: minus v itself / minus the partners sorted before v)
     I clo0 = w.cs, cln0 = w.ce - w.cs, clo1 = 0, cln1 = 0;
