@@ -15,6 +15,12 @@ for o in 1 0; do
   ncu -i $O/kq_o${o}.ncu-rep --page source --csv --print-source sass > $O/kq_o${o}_src.csv 2>/dev/null
 done
 python scripts/ncu_json.py $O/ncu_query_cfg3.json $O/kq_o1_raw.csv $O/kq_o0_raw.csv > $O/ncu_json.log 2>&1
+# config 5 (list output): the light count and emit kernels
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_query$" -c 2 \
+  -o $O/kq_cfg5 -f python scripts/prof_step.py --cfg 5 --reps 1 --order 0 > $O/kq_cfg5.log 2>&1
+ncu -i $O/kq_cfg5.ncu-rep --page raw --csv > $O/kq_cfg5_raw.csv 2>/dev/null
+python scripts/ncu_raw_summary.py $O/kq_cfg5_raw.csv > $O/kq_cfg5_summary.txt 2>&1
+rm -f $O/kq_cfg5.ncu-rep
 rm -f $O/phases.log
 for c in 1 2 3 4 5; do for o in 1 0; do timeout 300 python scripts/prof_step.py --cfg $c --reps 3 --order $o >> $O/phases.log 2>&1; done; done
 echo done
