@@ -13,7 +13,7 @@ if [ -n "$TESTK" ]; then
   env $TESTENV timeout 1500 python -m pytest tests -m gpu -x -q -k "$TESTK" > $O/ab_env_pytest.log 2>&1
   echo "pytest exit $?" >> $O/ab_env_pytest.log
 fi
-python - >> $O/ab_env.log <<'PY'
+python - > $O/ab_env_summary.txt <<'PY'
 import json
 for l in open('gpurun_out/ab_env.log'):
     if l.startswith('{'):
