@@ -100,6 +100,10 @@ def oracle_keys_dev(csr, n, dev):
 def test_config3_full_csr(rhg, cfg3):
     """All ~1e9 directed entries of config 3 vs orc_sweep_csr (Alg. 1 lines 13-21,
     PAPER.md:157-166; Eq. 3), in the bench's launch configuration."""
+    full_csr_compare(rhg, cfg3, {"test": "config3_full_csr"})
+
+
+def full_csr_compare(rhg, cfg3, tag):
     n, R = cfg3["n"], cfg3["R"]
     dev = torch.device("cuda")
     g = bench_launch(rhg, torch.from_numpy(cfg3["th"]).to(dev), torch.from_numpy(cfg3["r"]).to(dev),
@@ -123,7 +127,7 @@ def test_config3_full_csr(rhg, cfg3):
     excused = 0
     if not same:
         excused = check_disagreements(sorted_diff(gk, ok), sorted_diff(ok, gk), cfg3["csr"].ties)
-    record({"test": "config3_full_csr", "n": n, "directed_entries": int(m),
+    record({**tag, "n": n, "directed_entries": int(m),
             "oracle_directed_entries": int(ok.numel()), "oracle_near_tie_pairs": len(cfg3["csr"].ties),
             "disagreements": excused, "excused_as_near_ties": excused,
             "oracle_seconds": round(cfg3["t_orc"], 1)})
@@ -151,6 +155,26 @@ def test_config3_full_pairs(rhg, cfg3):
             "oracle_undirected_edges": int(ok.numel()),
             "oracle_near_tie_pairs": len(cfg3["csr"].ties), "disagreements": excused,
             "excused_as_near_ties": excused})
+
+
+EXTRA = [tuple(float(x) for x in c.split(",")) for c in
+         os.environ.get("RHG_FULLSIZE_EXTRA", "").split(";") if c.strip()]
+
+
+@pytest.mark.skipif(not EXTRA, reason="opt-in: RHG_FULLSIZE_EXTRA='n,kbar,gamma,seed;...'")
+@pytest.mark.parametrize("case", EXTRA or [None])
+def test_full_csr_other_seeds(rhg, orc, case):
+    """The config-3 comparison (all directed entries, bench launch configuration) on
+    other seeds / parameters at full scale; opt-in because each case costs the oracle
+    about half a minute.  Logged results: profiles/r02_near_ties.jsonl."""
+    n, kbar, gamma, seed = int(case[0]), case[1], case[2], int(case[3])
+    a = orc.alpha(gamma)
+    R = orc.target_radius(n, kbar, a)
+    th, r = orc.sample_points(n, a, R, seed)
+    t0 = time.perf_counter()
+    csr = orc.sweep_csr(th, r, R, cap_hint=int(1.05 * n * kbar))
+    full_csr_compare(rhg, dict(n=n, R=R, th=th, r=r, csr=csr, t_orc=time.perf_counter() - t0),
+                     {"test": "full_csr_other_seeds", "kbar": kbar, "gamma": gamma, "seed": seed})
 
 
 # --------------------------------------------------------------------------- config 5
