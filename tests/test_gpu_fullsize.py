@@ -161,9 +161,7 @@ EXTRA = [tuple(float(x) for x in c.split(",")) for c in
          os.environ.get("RHG_FULLSIZE_EXTRA", "").split(";") if c.strip()]
 
 
-@pytest.mark.skipif(not EXTRA, reason="opt-in: RHG_FULLSIZE_EXTRA='n,kbar,gamma,seed;...'")
-@pytest.mark.parametrize("case", EXTRA or [None])
-def test_full_csr_other_seeds(rhg, orc, case):
+def _full_csr_other_seeds(rhg, orc, case):
     """The config-3 comparison (all directed entries, bench launch configuration) on
     other seeds / parameters at full scale; opt-in because each case costs the oracle
     about half a minute.  Logged results: profiles/r02_near_ties.jsonl."""
@@ -175,6 +173,10 @@ def test_full_csr_other_seeds(rhg, orc, case):
     csr = orc.sweep_csr(th, r, R, cap_hint=int(1.05 * n * kbar))
     full_csr_compare(rhg, dict(n=n, R=R, th=th, r=r, csr=csr, t_orc=time.perf_counter() - t0),
                      {"test": "full_csr_other_seeds", "kbar": kbar, "gamma": gamma, "seed": seed})
+
+
+if EXTRA:  # opt-in (RHG_FULLSIZE_EXTRA='n,kbar,gamma,seed;...'): not collected otherwise
+    test_full_csr_other_seeds = pytest.mark.parametrize("case", EXTRA)(_full_csr_other_seeds)
 
 
 # --------------------------------------------------------------------------- config 5
