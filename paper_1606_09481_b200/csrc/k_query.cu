@@ -547,6 +547,9 @@ __device__ __forceinline__ double inv4s_of(double s) {
 #ifndef RHG_QK_MINB_COUNT
 #define RHG_QK_MINB_COUNT 8  // 64 registers (measured at config 3: 2.43 ms vs 2.49 ms with 56)
 #endif
+#ifndef RHG_QK_MINB_COUNT_LIST
+#define RHG_QK_MINB_COUNT_LIST 8  // count pass of the list output (its own instantiation)
+#endif
 #ifndef RHG_QK_MINB_EMIT
 #define RHG_QK_MINB_EMIT 9
 #endif
@@ -554,11 +557,15 @@ __device__ __forceinline__ double inv4s_of(double s) {
 #define RHG_QK_MINB_SEQ 7  // 72 registers: the eight sector registers of SecWriter
 #endif
 #ifndef RHG_QK_MINB_LIST
-#define RHG_QK_MINB_LIST 8  // list emit (COOP): no row stage, 64 registers
+#define RHG_QK_MINB_LIST 10  // list emit (COOP), sample ids: no row stage; 48 registers (config 5
+                             // emit 6.24 ms at 8 blocks / 64 registers, 6.13 at 9, 6.07 at 10)
+#endif
+#ifndef RHG_QK_MINB_LIST_SEQ
+#define RHG_QK_MINB_LIST_SEQ 9  // list emit, vertex_order 1: 56 registers (5.72 ms at 8, 5.59 at 9, 5.70 at 10)
 #endif
 template <int MODE, int FMT, bool WIDE, bool SEQ>
-__global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? RHG_QK_MINB_COUNT
-                                              : (FMT == RHG_EDGES_UNDIRECTED ? RHG_QK_MINB_LIST
+__global__ void __launch_bounds__(QK_THREADS, MODE == QM_COUNT ? (FMT == RHG_EDGES_UNDIRECTED ? RHG_QK_MINB_COUNT_LIST : RHG_QK_MINB_COUNT)
+                                              : (FMT == RHG_EDGES_UNDIRECTED ? (SEQ ? RHG_QK_MINB_LIST_SEQ : RHG_QK_MINB_LIST)
                                               : (SEQ ? RHG_QK_MINB_SEQ : RHG_QK_MINB_EMIT)))
     k_query(const QueryArgs A, const __grid_constant__ BandConst bc) {
   using I = typename std::conditional<WIDE, int64_t, int32_t>::type;
